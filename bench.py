@@ -1,0 +1,319 @@
+"""Benchmark: solution paths tracked per second (complex fp64) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Workload (BASELINE.json configs[4], the 3.6M-path config named by the north
+star): C5, the n=10 cyclic-support system, total-degree homotopy, 10! =
+3,628,800 paths.  One step = every path tracked t: 0 -> 1 with the
+reference's TrackParams, endpoints finished (damped Newton, SVD condition,
+double-double polish of ill-conditioned ones), and -- for N > 1 -- the finite
+endpoints gathered to rank 0 over NCCL.  Ranks own equal contiguous shards of
+the path index space (strong scaling: total work fixed) and generate their
+own starts on the device.
+
+value : paths/s with everything device-resident (CUDA events on the stream,
+        max over ranks).
+e2e   : the same through the C-ABI with host buffers: start points copied
+        from pinned host memory, endpoints/statuses copied back, per step.
+cpu_baseline / --impl reference : the oracle port of the reference tracker
+        (oracle/nid_oracle.py) on the host's cores over a seeded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "solution paths tracked/sec (complex fp64)"
+UNIT = "paths/s"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------- CPU legs (oracle)
+
+
+def cpu_sample(prob, count: int, seed: int) -> np.ndarray:
+    from paper_1804_03807_b200 import systems
+
+    idx = np.sort(np.random.default_rng(seed).choice(prob.paths, size=count, replace=False))
+    return np.concatenate([systems.total_degree_starts(prob.degrees, int(i), 1) for i in idx])
+
+
+def run_oracle(prob, starts: np.ndarray, procs: int) -> float:
+    """Track `starts` with the oracle port on `procs` processes; returns seconds."""
+    from oracle import nid_oracle as O
+
+    h = O.LinearHomotopy(prob.start, prob.target, prob.gamma)
+    t0 = time.perf_counter()
+    O.track_many(h, list(starts), O.TrackParams(), procs=procs)
+    return time.perf_counter() - t0
+
+
+def reference_arm(args, prob):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = host_cores()
+    per_step = args.ref_sample
+    starts = cpu_sample(prob, per_step * (args.steps + args.warmup), 7)
+    for w in range(args.warmup):
+        run_oracle(prob, starts[w * per_step:(w + 1) * per_step], cores)
+    tot = 0.0
+    for k in range(args.steps):
+        lo = (args.warmup + k) * per_step
+        tot += run_oracle(prob, starts[lo:lo + per_step], cores)
+    value = per_step * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": "C5 cyclic-support n=10, total-degree homotopy (3,628,800 paths)", "paths": prob.paths,
+                   "sample_paths_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{per_step} seeded uniform C5 path indices per step, oracle/nid_oracle.py "
+                                   f"(numpy restatement of nidpipe.tracker.track) on {cores} processes"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self, device: int):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+        except Exception:
+            return None
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 9 and r[0].strip() == str(device)]
+        if not rows:
+            return None
+        sm = np.array([float(r[1]) for r in rows])
+        smax = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        load = sm[sm > 0.5 * smax] if np.any(sm > 0.5 * smax) else sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+    try:
+        for line in open(p):
+            d = json.loads(line)
+            if "fp64_tflops_sustained" in d:
+                return float(d["fp64_tflops_sustained"]), "measured DFMA peak on this pool's B200 (tools/fp64_peak.cu)"
+    except Exception:
+        pass
+    return 37.2, "nominal 148 SM x 64 FMA x 2 x 1.965 GHz (no measurement found)"
+
+
+def native_arm(args, prob):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1804_03807_b200 import flops, tracker
+    from paper_1804_03807_b200.homotopy import LinearHomotopy, TrackParams
+    from paper_1804_03807_b200.parallel import DistContext, gather_finite
+
+    ctx = DistContext.from_env(args.gpus)
+    torch.cuda.set_device(ctx.local_rank)
+    dev = torch.device("cuda", ctx.local_rank)
+    n = prob.n
+    P = prob.paths
+    lo, hi = ctx.shard(P)
+    Pl = hi - lo
+    h = LinearHomotopy(prob.start, prob.target, prob.gamma)
+    params = TrackParams()
+    fm = flops.flop_model(h.lowered())
+
+    x_end = torch.empty((Pl, n, 2), dtype=torch.float64, device=dev)
+    status = torch.empty(Pl, dtype=torch.int8, device=dev)
+    steps_t = torch.empty(Pl, dtype=torch.int32, device=dev)
+    treach = torch.empty(Pl, dtype=torch.float64, device=dev)
+    resid = torch.empty(Pl, dtype=torch.float64, device=dev)
+    cond = torch.empty(Pl, dtype=torch.float64, device=dev)
+    reg = torch.empty(Pl, dtype=torch.int8, device=dev)
+    outp = {"x_end": x_end.data_ptr(), "status": status.data_ptr(), "steps": steps_t.data_ptr(),
+            "t_reached": treach.data_ptr(), "residual": resid.data_ptr(), "condition": cond.data_ptr(),
+            "regular": reg.data_ptr()}
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        flush.fill_(1.0)
+        c = tracker.track_batch_device(h, params, Pl, outp, degrees=prob.degrees, first_index=lo,
+                                       stream=stream.cuda_stream)
+        if ctx.world > 1:
+            gather_finite(ctx, x_end, status)
+        return c
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    counters = []
+    with ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_bench_r{ctx.rank}.csv")
+                      if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp/nid_clocks.csv") as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            counters.append(step())
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ctx.barrier()
+    ms = e0.elapsed_time(e1)
+    ms_max = ctx.max_over_ranks(ms)
+    value = P * args.steps / (ms_max / 1000.0)
+
+    # per-rank kernel accounting (track kernel = the dominant kernel)
+    ev = np.mean([c["evals"] for c in counters])
+    jc = np.mean([c["jacs"] for c in counters])
+    sc = np.mean([c["scales"] for c in counters])
+    k_ms = float(np.mean([c["kernel_ms_track"] for c in counters]))
+    e_ms = float(np.mean([c["kernel_ms_endpoint"] for c in counters]))
+    flop = fm.total(ev, jc, sc)
+    achieved = flop / (k_ms / 1000.0) / 1e12
+    peak, peak_src = fp64_peak()
+    st = status.cpu().numpy()
+    finite_local = int(np.sum((st == 0) | (st == 2)))
+    finite = ctx.sum_over_ranks(finite_local)
+
+    # e2e through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        from paper_1804_03807_b200 import systems
+
+        X0 = torch.empty((Pl, n, 2), dtype=torch.float64).pin_memory()
+        X0.numpy().view(np.complex128).reshape(Pl, n)[:] = systems.total_degree_starts(prob.degrees, lo, Pl)
+        pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory()  # noqa: E731
+        ho = tracker.TrackResults(pin((Pl, n, 2), torch.float64).numpy().view(np.complex128).reshape(Pl, n),
+                                  pin(Pl, torch.int8).numpy(), pin(Pl, torch.int32).numpy(),
+                                  pin(Pl, torch.float64).numpy(), pin(Pl, torch.float64).numpy(),
+                                  pin(Pl, torch.float64).numpy(), pin(Pl, torch.int8).numpy(), {})
+        x0v = X0.numpy().view(np.complex128).reshape(Pl, n)
+        tracker.track_batch(h, x0v, params, out=ho)  # warm
+        ctx.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            r = tracker.track_batch(h, x0v, params, out=ho)
+            _ = int(np.sum(r.succeeded))  # the step's result read on the host
+        torch.cuda.synchronize()
+        dt = ctx.max_over_ranks(time.perf_counter() - t0)
+        h2d = Pl * n * 16
+        d2h = Pl * (n * 16 + 1 + 4 + 8 + 8 + 8 + 1) + 64
+        e2e = {"value": P * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d * ctx.world,
+               "d2h_bytes_per_step": d2h * ctx.world, "steps": args.e2e_steps,
+               "timing": "wall clock around the public C-ABI call (it synchronizes), max over ranks"}
+
+    cpu = None
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        starts = cpu_sample(prob, args.cpu_sample, 11)
+        secs = run_oracle(prob, starts, cores)
+        cpu = {"value": args.cpu_sample / secs, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_sample} seeded uniform C5 path indices, oracle/nid_oracle.py "
+                         f"(numpy restatement of nidpipe.tracker.track) on {cores} processes"}
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "track_traffic_r01.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if ctx.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": "C5 cyclic-support n=10, total-degree homotopy (BASELINE configs[4])",
+                       "paths": P, "n": n, "seed": 5, "track_params": "reference defaults (tracker.py:113-127)",
+                       "l2": "256 MB device fill before every step (> 126 MB L2); endpoint outputs 580 MB",
+                       "finite_endpoints": finite, "parallelism": f"path shards x{ctx.world}"},
+            "clocks": clk.summary(ctx.local_rank),
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "track_kernel<10>",
+                         "peak_source": peak_src,
+                         "algorithmic_flop_per_launch": flop, "kernel_ms_per_launch": k_ms,
+                         "endpoint_kernel_ms_per_launch": e_ms, "share_of_step": k_ms / (ms / args.steps),
+                         "counts_per_path": {"eval": ev / Pl, "jac": jc / Pl, "scale": sc / Pl},
+                         "flop_model": fm.as_dict()},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=480)
+    ap.add_argument("--ref-sample", type=int, default=160)
+    args = ap.parse_args()
+    from paper_1804_03807_b200 import configs
+
+    prob = configs.c5()
+    if args.impl == "reference":
+        return reference_arm(args, prob)
+    return native_arm(args, prob)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

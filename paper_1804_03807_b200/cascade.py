@@ -1,0 +1,203 @@
+"""Top-dimensional continuation and the cascade of embedded homotopies on the
+GPU (mode="gpu"), with the reference's signatures and records
+(pkg/src/nidpipe/cascade.py:47-337).
+
+Every stage batches all of its paths into one `track_batch` launch (the
+reference fans them out through `work_crew`), and refines + classifies all
+endpoints of a level in one `refine_batch` launch.
+
+Difference from the reference, by scope: `solve_top`
+starts from the total-degree system G_i = x_i^{d_i} - 1 instead of the
+polyhedral random-coefficient system; gamma is the reference's own draw
+`stream(seed, GAMMA)` (cascade.py:226).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import rng as rngmod
+from .homotopy import LinearHomotopy, TrackParams
+from .polys import PolySystem, make_poly, variable_poly
+from .systems import EmbeddedSystem, total_degree_start
+from .tracker import (
+    AT_INFINITY,
+    NONZERO_SLACK,
+    ZERO_SLACK,
+    PathResult,
+    Solution,
+    TrackResults,
+    refine_batch,
+    track_batch,
+)
+
+GPU_MODES = ("gpu",)
+
+
+def _check_mode(mode: str):
+    if mode not in GPU_MODES:
+        raise ValueError(f"mode {mode!r}: this framework implements the GPU path only (mode='gpu'); "
+                         "the CPU work crew is the reference's")
+
+
+@dataclass
+class TopStats:
+    """cascade.py:47-59"""
+
+    cells: int = 0
+    mixed_volume: int = 0
+    start_paths: int = 0
+    start_failures: int = 0
+    continuation_paths: int = 0
+    at_infinity: int = 0
+    finite: int = 0
+    failures: int = 0
+    lifting_attempt: int = 0
+    time_start_system: float = 0.0
+    time_continuation: float = 0.0
+
+
+@dataclass
+class CascadeLevel:
+    """cascade.py:62-88"""
+
+    dimension: int
+    embedding: EmbeddedSystem
+    starts: int
+    at_infinity: int
+    zero_slack: list = field(default_factory=list)
+    nonzero_slack: list = field(default_factory=list)
+    failures: int = 0
+
+    @property
+    def counts(self) -> dict:
+        return {"dimension": self.dimension, "starts": self.starts, "at_infinity": self.at_infinity,
+                "zero_slack": len(self.zero_slack), "nonzero_slack": len(self.nonzero_slack),
+                "failures": self.failures}
+
+
+@dataclass
+class WitnessSuperset:
+    """cascade.py:91-107"""
+
+    levels: list
+    embedding: EmbeddedSystem
+    seed: int
+
+    def candidates(self, dimension: int) -> list:
+        for lv in self.levels:
+            if lv.dimension == dimension:
+                return lv.zero_slack
+        return []
+
+    @property
+    def stage_counts(self) -> list:
+        return [lv.counts for lv in self.levels]
+
+
+def top_homotopy(emb: EmbeddedSystem, seed: int | None = None) -> tuple[LinearHomotopy, tuple]:
+    seed = emb.seed if seed is None else seed
+    system = emb.system if emb.k > 0 else emb.base
+    g = total_degree_start(system)
+    gamma = rngmod.gamma_for(seed)
+    return LinearHomotopy(g, system, gamma), tuple(system.degrees())
+
+
+def solve_top(emb: EmbeddedSystem, p: int = 1, seed: int | None = None, params: TrackParams = TrackParams(),
+              mode: str = "gpu", cell_log: list | None = None, return_arrays: bool = False):
+    """Continuation from the total-degree start to the embedded system
+    (cascade.py:214-246).  Returns (results, TopStats)."""
+    _check_mode(mode)
+    h, degrees = top_homotopy(emb, seed)
+    total = int(np.prod(degrees, dtype=np.int64))
+    stats = TopStats(start_paths=total)
+    t0 = time.perf_counter()
+    res = track_batch(h, None, params, degrees=degrees, count=total)
+    stats.time_continuation = time.perf_counter() - t0
+    c = res.counts()
+    stats.continuation_paths = total
+    stats.at_infinity = c["at_infinity"]
+    stats.finite = c["converged"] + c["singular_endpoint"]
+    stats.failures = c["failed"]
+    if stats.continuation_paths and stats.finite == 0:
+        raise RuntimeError("all continuation paths failed")
+    return (res if return_arrays else res.path_results()), stats
+
+
+def _classify_arrays(x: np.ndarray, status_ok: np.ndarray, n_at_inf: int, n_fail: int, emb_level: EmbeddedSystem,
+                     dimension: int, params: TrackParams, starts: int) -> CascadeLevel:
+    lv = CascadeLevel(dimension, emb_level, starts=starts, at_infinity=n_at_inf, failures=n_fail)
+    system = emb_level.system if emb_level.k else emb_level.base
+    pts = x[status_ok]
+    if len(pts):
+        rr = refine_batch(system, pts, tol=1e-13, max_iters=6, n_original=emb_level.n_original,
+                          infinity_threshold=params.infinity_threshold)
+        for i in range(len(pts)):
+            sol = rr.solution(i, with_slack=True)
+            if sol.slack_class == AT_INFINITY:
+                lv.at_infinity += 1
+            elif sol.slack_class == ZERO_SLACK:
+                lv.zero_slack.append(sol)
+            else:
+                lv.nonzero_slack.append(sol)
+    return lv
+
+
+def _classify_level(results, emb_level: EmbeddedSystem, dimension: int, params: TrackParams) -> CascadeLevel:
+    """Refine + three-way classification of tracked paths (cascade.py:249-277)."""
+    if isinstance(results, TrackResults):
+        ok = results.succeeded
+        c = results.counts()
+        return _classify_arrays(results.x, ok, c["at_infinity"], c["failed"], emb_level, dimension, params,
+                                len(results))
+    n = emb_level.nvars
+    at_inf = sum(1 for r in results if r.status == AT_INFINITY)
+    ok = np.array([r.status != AT_INFINITY and r.succeeded and r.endpoint is not None for r in results], bool)
+    fails = len(results) - at_inf - int(ok.sum())
+    x = np.zeros((len(results), n), np.complex128)
+    for i, r in enumerate(results):
+        if ok[i]:
+            x[i] = r.endpoint.coordinates
+    return _classify_arrays(x, ok, at_inf, fails, emb_level, dimension, params, len(results))
+
+
+def _slack_removal_homotopy(emb: EmbeddedSystem, gamma: complex) -> LinearHomotopy:
+    """Last hyperplane row x gamma deforms into z_d = 0 (cascade.py:280-293)."""
+    system = emb.system
+    nv = system.nvars
+    rows_s = list(system.polys)
+    rows_t = list(system.polys)
+    rows_s[-1] = make_poly(nv, [(e, gamma * c) for e, c in rows_s[-1].terms])
+    rows_t[-1] = variable_poly(nv, nv - 1)
+    return LinearHomotopy(PolySystem(nv, tuple(rows_s), system.names), PolySystem(nv, tuple(rows_t), system.names))
+
+
+def cascade_step(level: CascadeLevel, p: int = 1, params: TrackParams = TrackParams(), mode: str = "gpu") -> CascadeLevel:
+    """Track the level's nonzero-slack solutions one dimension down (cascade.py:296-322)."""
+    _check_mode(mode)
+    if level.dimension < 1:
+        raise ValueError("cannot cascade below dimension 0")
+    emb = level.embedding
+    nxt = emb.level(emb.k - 1)
+    if not level.nonzero_slack:
+        return CascadeLevel(level.dimension - 1, nxt, starts=0, at_infinity=0)
+    gamma = rngmod.gamma_for(emb.seed, level.dimension)
+    h = _slack_removal_homotopy(emb, gamma)
+    starts = np.array([s.coordinates for s in level.nonzero_slack])
+    res = track_batch(h, starts, params)
+    c = res.counts()
+    return _classify_arrays(res.x[:, :-1], res.succeeded, c["at_infinity"], c["failed"], nxt,
+                            level.dimension - 1, params, len(res))
+
+
+def run_cascade(top_results, emb: EmbeddedSystem, p: int = 1, params: TrackParams = TrackParams(),
+                mode: str = "gpu") -> WitnessSuperset:
+    """cascade.py:325-337"""
+    _check_mode(mode)
+    levels = [_classify_level(top_results, emb, emb.k, params)]
+    while levels[-1].dimension > 0:
+        levels.append(cascade_step(levels[-1], p, params, mode))
+    return WitnessSuperset(levels, emb, emb.seed)

@@ -1,0 +1,532 @@
+// libnid.so: the C-ABI boundary (declared in include/nid.h).
+// Host-side plumbing only: uploads lowered homotopies, stages host buffers,
+// sizes the persistent grids and dispatches to the per-size kernels.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "aux_kernels.cuh"
+#include "endpoint.cuh"
+#include "launch.h"
+#include "track.cuh"
+
+static thread_local std::string g_err;
+static NidCounters g_counters = {};
+static int g_device = -1;
+
+#define FAIL(msg)          \
+  do {                     \
+    g_err = (msg);         \
+    return 1;              \
+  } while (0)
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);                          \
+      return 2;                                                                           \
+    }                                                                                     \
+  } while (0)
+
+struct NidHomotopy {
+  int n, nterms, nparam, maxdeg;
+  cd gamma;
+  int* row_off;
+  uint4* expo;
+  cd *cs, *ct;
+  double *acs, *act;
+  int8_t* pslot;
+  HomDev dev() const {
+    HomDev h;
+    h.n = n;
+    h.nterms = nterms;
+    h.nparam = nparam;
+    h.maxdeg = maxdeg;
+    h.row_off = row_off;
+    h.expo = expo;
+    h.cs = cs;
+    h.ct = ct;
+    h.acs = acs;
+    h.act = act;
+    h.pslot = pslot;
+    h.gamma = gamma;
+    return h;
+  }
+};
+
+// grow-only device workspace slots
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+static Buf g_bufs[32];
+template <class T>
+static T* ws(int slot, size_t count) {
+  size_t bytes = count * sizeof(T) + 16;
+  Buf& b = g_bufs[slot];
+  if (b.cap < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) return nullptr;
+    b.cap = bytes;
+  }
+  return reinterpret_cast<T*>(b.p);
+}
+
+#define NID_TABLE(fn)                                                                                    \
+  {nullptr,  nid::fn##1,  nid::fn##2,  nid::fn##3,  nid::fn##4,  nid::fn##5,  nid::fn##6, nid::fn##7, \
+   nid::fn##8, nid::fn##9, nid::fn##10, nid::fn##11, nid::fn##12, nid::fn##13, nid::fn##14, nid::fn##15, \
+   nid::fn##16}
+
+typedef int (*TrackFn)(const TrackArgs&, int, cudaStream_t);
+typedef int (*EndpointFn)(const EndpointArgs&, int, cudaStream_t);
+typedef int (*RefineFn)(const RefineArgs&, int, cudaStream_t);
+typedef int (*DDRefineFn)(const DDRefineArgs&, int, cudaStream_t);
+typedef int (*EvalFn)(const EvalArgs&, int, cudaStream_t);
+typedef int (*NewtonFn)(const NewtonArgs&, int, cudaStream_t);
+typedef int (*RegsFn)();
+static const TrackFn k_track[17] = NID_TABLE(launch_track_);
+static const EndpointFn k_endpoint[17] = NID_TABLE(launch_endpoint_);
+static const RefineFn k_refine[17] = NID_TABLE(launch_refine_);
+static const DDRefineFn k_ddrefine[17] = NID_TABLE(launch_ddrefine_);
+static const EvalFn k_eval[17] = NID_TABLE(launch_eval_);
+static const NewtonFn k_newton[17] = NID_TABLE(launch_newton_);
+static const RegsFn k_regs[17] = NID_TABLE(track_regs_);
+
+static int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+// number of 128-thread blocks for a grid-stride group kernel over P points
+static int grid_for(long long P, int n, int per_sm) {
+  long long groups_per_block = 4 * (32 / n);
+  long long need = (P + groups_per_block - 1) / groups_per_block;
+  long long cap = (long long)sm_count() * per_sm;
+  if (need > cap) need = cap;
+  return need < 1 ? 1 : (int)need;
+}
+
+static long long groups_of(int blocks, int n) { return (long long)blocks * 4 * (32 / n); }
+
+extern "C" {
+
+const char* nid_last_error(void) { return g_err.c_str(); }
+
+int nid_device_count(int* count) {
+  CK(cudaGetDeviceCount(count));
+  return 0;
+}
+
+int nid_init(int device) {
+  CK(cudaSetDevice(device));
+  CK(cudaFree(0));
+  g_device = device;
+  return 0;
+}
+
+int nid_shutdown(void) {
+  for (auto& b : g_bufs) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  return 0;
+}
+
+int nid_track_regs(int n) {
+  if (n < 1 || n > 16) return -1;
+  return k_regs[n]();
+}
+
+int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
+  if (!d || !out) FAIL("null argument");
+  if (d->n < 1 || d->n > NID_MAX_VARS) FAIL("n must be in 1..16");
+  if (d->nterms < 0) FAIL("negative term count");
+  const int n = d->n, T = d->nterms;
+  std::vector<int> off(d->row_off, d->row_off + n + 1);
+  if (off[0] != 0 || off[n] != T) FAIL("row offsets do not cover the term table");
+  for (int i = 0; i < n; ++i)
+    if (off[i + 1] < off[i]) FAIL("row offsets not monotone");
+  std::vector<double> acs(T), act(T);
+  int maxdeg = 0;
+  for (int k = 0; k < T; ++k) {
+    acs[k] = hypot(d->coef_start[2 * k], d->coef_start[2 * k + 1]);
+    act[k] = hypot(d->coef_target[2 * k], d->coef_target[2 * k + 1]);
+    for (int v = 0; v < NID_MAX_VARS; ++v) {
+      int a = d->expo[k * NID_MAX_VARS + v];
+      if (v >= n && a) FAIL("exponent set on a variable >= n");
+      if (a > maxdeg) maxdeg = a;
+    }
+  }
+  NidHomotopy* h = new NidHomotopy();
+  h->n = n;
+  h->nterms = T;
+  h->nparam = d->nparam;
+  h->maxdeg = maxdeg;
+  h->gamma = cd{d->gamma_re, d->gamma_im};
+  const size_t Tp = T > 0 ? T : 1;
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMalloc(&h->row_off, (n + 1) * sizeof(int));
+  e = e ? e : cudaMalloc(&h->expo, Tp * sizeof(uint4));
+  e = e ? e : cudaMalloc(&h->cs, Tp * sizeof(cd));
+  e = e ? e : cudaMalloc(&h->ct, Tp * sizeof(cd));
+  e = e ? e : cudaMalloc(&h->acs, Tp * sizeof(double));
+  e = e ? e : cudaMalloc(&h->act, Tp * sizeof(double));
+  h->pslot = nullptr;
+  if (!e && d->param_slot) e = cudaMalloc(&h->pslot, Tp);
+  if (!e) e = cudaMemcpy(h->row_off, off.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice);
+  if (!e && T) e = cudaMemcpy(h->expo, d->expo, T * sizeof(uint4), cudaMemcpyHostToDevice);
+  if (!e && T) e = cudaMemcpy(h->cs, d->coef_start, T * sizeof(cd), cudaMemcpyHostToDevice);
+  if (!e && T) e = cudaMemcpy(h->ct, d->coef_target, T * sizeof(cd), cudaMemcpyHostToDevice);
+  if (!e && T) e = cudaMemcpy(h->acs, acs.data(), T * sizeof(double), cudaMemcpyHostToDevice);
+  if (!e && T) e = cudaMemcpy(h->act, act.data(), T * sizeof(double), cudaMemcpyHostToDevice);
+  if (!e && T && d->param_slot) e = cudaMemcpy(h->pslot, d->param_slot, T, cudaMemcpyHostToDevice);
+  if (e) {
+    g_err = std::string("homotopy upload: ") + cudaGetErrorString(e);
+    delete h;
+    return 2;
+  }
+  *out = h;
+  return 0;
+}
+
+int nid_homotopy_destroy(NidHomotopy* h) {
+  if (!h) return 0;
+  cudaFree(h->row_off);
+  cudaFree(h->expo);
+  cudaFree(h->cs);
+  cudaFree(h->ct);
+  cudaFree(h->acs);
+  cudaFree(h->act);
+  if (h->pslot) cudaFree(h->pslot);
+  delete h;
+  return 0;
+}
+
+int nid_last_counters(NidCounters* c) {
+  if (!c) FAIL("null argument");
+  *c = g_counters;
+  return 0;
+}
+
+// slot map for the workspace cache
+enum {
+  W_STARTS = 0, W_PARAMS, W_XEND, W_STATUS, W_STEPS, W_TREACH, W_RESID, W_COND, W_REG,
+  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL
+};
+
+int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
+                    long long first_index, const int32_t* degrees, const double* params, int param_div,
+                    NidPathOut* out, int device_io, void* stream) {
+  if (!h || !prm || !out) FAIL("null argument");
+  if (P < 0) FAIL("negative path count");
+  const int n = h->n;
+  cudaStream_t s = (cudaStream_t)stream;
+  memset(&g_counters, 0, sizeof(g_counters));
+  if (P == 0) return 0;
+  if (!starts && !degrees) FAIL("need explicit starts or total-degree degrees");
+  if (h->nparam > 0 && !params) FAIL("homotopy has per-path parameters but none were given");
+  if (param_div < 1) param_div = 1;
+
+  const cd* d_starts = nullptr;
+  const cd* d_params = nullptr;
+  cd* d_x;
+  int8_t *d_st, *d_reg;
+  int* d_steps;
+  double *d_tr, *d_res, *d_cond;
+  if (device_io) {
+    d_starts = (const cd*)starts;
+    d_params = (const cd*)params;
+    d_x = (cd*)out->x_end;
+    d_st = out->status;
+    d_steps = out->steps;
+    d_tr = out->t_reached;
+    d_res = out->residual;
+    d_cond = out->condition;
+    d_reg = out->regular;
+  } else {
+    if (starts) {
+      cd* p = ws<cd>(W_STARTS, (size_t)P * n);
+      if (!p) FAIL("out of device memory (starts)");
+      CK(cudaMemcpyAsync(p, starts, (size_t)P * n * sizeof(cd), cudaMemcpyHostToDevice, s));
+      d_starts = p;
+    }
+    if (params && h->nparam > 0) {
+      size_t np = ((size_t)(P - 1) / param_div + 1) * h->nparam;
+      cd* p = ws<cd>(W_PARAMS, np);
+      if (!p) FAIL("out of device memory (params)");
+      CK(cudaMemcpyAsync(p, params, np * sizeof(cd), cudaMemcpyHostToDevice, s));
+      d_params = p;
+    }
+    d_x = ws<cd>(W_XEND, (size_t)P * n);
+    d_st = ws<int8_t>(W_STATUS, P);
+    d_steps = ws<int>(W_STEPS, P);
+    d_tr = ws<double>(W_TREACH, P);
+    d_res = ws<double>(W_RESID, P);
+    d_cond = ws<double>(W_COND, P);
+    d_reg = ws<int8_t>(W_REG, P);
+    if (!d_x || !d_st || !d_steps || !d_tr || !d_res || !d_cond || !d_reg) FAIL("out of device memory (outputs)");
+  }
+  unsigned long long* d_cnt = ws<unsigned long long>(W_COUNT, 8);
+  if (!d_cnt) FAIL("out of device memory (counters)");
+  CK(cudaMemsetAsync(d_cnt, 0, 8 * sizeof(unsigned long long), s));
+
+  TrackArgs a;
+  memset(&a, 0, sizeof(a));
+  a.H = h->dev();
+  a.prm = *prm;
+  a.P = P;
+  a.first_index = first_index;
+  a.starts = d_starts;
+  for (int v = 0; v < NID_MAX_VARS; ++v) a.deg[v] = (degrees && v < n) ? degrees[v] : 1;
+  if (!starts)
+    for (int v = 0; v < n; ++v)
+      if (a.deg[v] < 1) FAIL("total-degree start degrees must be >= 1");
+  a.params = d_params;
+  a.param_div = param_div;
+  a.next = d_cnt + 7;
+  a.x_end = d_x;
+  a.status = d_st;
+  a.steps = d_steps;
+  a.t_reached = d_tr;
+  a.resid = d_res;
+  a.counters = d_cnt;
+  // lstsq scratch for every resident group
+  const int max_blocks = sm_count() * 8;
+  a.scratch = ws<cd>(W_SCR, (size_t)groups_of(max_blocks, n) * (3 * n * n + 2 * n));
+  if (!a.scratch) FAIL("out of device memory (scratch)");
+
+  cudaEvent_t e0, e1, e2;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&e2));
+  CK(cudaEventRecord(e0, s));
+  k_track[n](a, max_blocks, s);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e1, s));
+
+  EndpointArgs E;
+  memset(&E, 0, sizeof(E));
+  E.H = h->dev();
+  E.P = P;
+  E.dd_steps = prm->dd_refine_singular > 0 ? (prm->dd_refine_singular > 14 ? prm->dd_refine_singular : 14) : 0;
+  E.params = d_params;
+  E.param_div = param_div;
+  E.x_end = d_x;
+  E.status = d_st;
+  E.resid = d_res;
+  E.cond = d_cond;
+  E.regular = d_reg;
+  E.counters = d_cnt + 4;
+  int eblocks = grid_for(P, n, 4);
+  E.ddscratch = ws<cdd>(W_DDSCR, (size_t)groups_of(eblocks, n) * (2 * n * n + 4 * n));
+  E.cscratch = ws<cd>(W_TOL, (size_t)groups_of(eblocks, n) * (2 * n * n));
+  if (!E.ddscratch || !E.cscratch) FAIL("out of device memory (endpoint scratch)");
+  k_endpoint[n](E, eblocks, s);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e2, s));
+
+  if (!device_io) {
+    CK(cudaMemcpyAsync(out->x_end, d_x, (size_t)P * n * sizeof(cd), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out->status, d_st, P, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out->steps, d_steps, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out->t_reached, d_tr, P * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out->residual, d_res, P * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out->condition, d_cond, P * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out->regular, d_reg, P, cudaMemcpyDeviceToHost, s));
+  }
+  unsigned long long hc[8];
+  CK(cudaMemcpyAsync(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  float ms1 = 0.f, ms2 = 0.f;
+  cudaEventElapsedTime(&ms1, e0, e1);
+  cudaEventElapsedTime(&ms2, e1, e2);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  g_counters.evals = (long long)hc[0];
+  g_counters.jacs = (long long)hc[1];
+  g_counters.scales = (long long)hc[2];
+  g_counters.lstsq_fallbacks = (long long)hc[3];
+  g_counters.dd_polished = (long long)hc[4];
+  g_counters.paths = P;
+  g_counters.kernel_ms_track = ms1;
+  g_counters.kernel_ms_endpoint = ms2;
+  return 0;
+}
+
+int nid_eval_batch(NidHomotopy* h, int P, const double* x, const double* t, const double* params, int param_div,
+                   double* H, double* J, double* scale) {
+  if (!h || !x || !t || !H || !J || !scale) FAIL("null argument");
+  if (P <= 0) return 0;
+  const int n = h->n;
+  if (param_div < 1) param_div = 1;
+  cd* dx = ws<cd>(W_X, (size_t)P * n);
+  double* dt = ws<double>(W_T, P);
+  cd* dH = ws<cd>(W_H, (size_t)P * n);
+  cd* dJ = ws<cd>(W_J, (size_t)P * n * n);
+  double* ds = ws<double>(W_SCALE, P);
+  if (!dx || !dt || !dH || !dJ || !ds) FAIL("out of device memory");
+  cd* dp = nullptr;
+  if (h->nparam > 0) {
+    if (!params) FAIL("homotopy has per-path parameters but none were given");
+    size_t np = ((size_t)(P - 1) / param_div + 1) * h->nparam;
+    dp = ws<cd>(W_PARAMS, np);
+    CK(cudaMemcpy(dp, params, np * sizeof(cd), cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemcpy(dx, x, (size_t)P * n * sizeof(cd), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dt, t, P * sizeof(double), cudaMemcpyHostToDevice));
+  EvalArgs E;
+  E.H = h->dev();
+  E.P = P;
+  E.x = dx;
+  E.t = dt;
+  E.params = dp;
+  E.param_div = param_div;
+  E.Hout = dH;
+  E.Jout = dJ;
+  E.scale = ds;
+  k_eval[n](E, grid_for(P, n, 8), 0);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(H, dH, (size_t)P * n * sizeof(cd), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(J, dJ, (size_t)P * n * n * sizeof(cd), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(scale, ds, P * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int nid_newton_step_batch(int n, int P, const double* J, const double* r, double* dx) {
+  if (!J || !r || !dx) FAIL("null argument");
+  if (n < 1 || n > 16) FAIL("n must be in 1..16");
+  if (P <= 0) return 0;
+  cd* dJ = ws<cd>(W_J, (size_t)P * n * n);
+  cd* dr = ws<cd>(W_H, (size_t)P * n);
+  cd* dd_ = ws<cd>(W_X, (size_t)P * n);
+  int blocks = grid_for(P, n, 8);
+  cd* sc = ws<cd>(W_SCR, (size_t)groups_of(blocks, n) * (3 * n * n + 2 * n));
+  if (!dJ || !dr || !dd_ || !sc) FAIL("out of device memory");
+  CK(cudaMemcpy(dJ, J, (size_t)P * n * n * sizeof(cd), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dr, r, (size_t)P * n * sizeof(cd), cudaMemcpyHostToDevice));
+  NewtonArgs A;
+  A.P = P;
+  A.J = dJ;
+  A.r = dr;
+  A.dx = dd_;
+  A.cscratch = sc;
+  k_newton[n](A, blocks, 0);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(dx, dd_, (size_t)P * n * sizeof(cd), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int nid_svd_batch(int m, int n, int P, const double* A, double* sv) {
+  if (!A || !sv) FAIL("null argument");
+  if (n < 1 || n > 16 || m < n || m > 32) FAIL("need 1 <= n <= 16 and n <= m <= 32");
+  if (P <= 0) return 0;
+  cd* dA = ws<cd>(W_J, (size_t)P * m * n);
+  cd* sc = ws<cd>(W_SCR, (size_t)P * m * n);
+  double* ds = ws<double>(W_SCALE, (size_t)P * n);
+  if (!dA || !sc || !ds) FAIL("out of device memory");
+  CK(cudaMemcpy(dA, A, (size_t)P * m * n * sizeof(cd), cudaMemcpyHostToDevice));
+  svd_kernel<<<(P + 127) / 128, 128>>>(m, n, P, dA, sc, ds);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(sv, ds, (size_t)P * n * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int nid_refine_batch(NidHomotopy* h, int P, double* x, double tol, int iters, int n_original,
+                     double infinity_threshold, double* residual, double* condition, int8_t* regular,
+                     int32_t* rank, int8_t* slack_class) {
+  if (!h || !x || !residual || !condition || !regular || !rank || !slack_class) FAIL("null argument");
+  if (h->nparam > 0) FAIL("refine does not take per-path parameters");
+  if (P <= 0) return 0;
+  const int n = h->n;
+  int blocks = grid_for(P, n, 4);
+  cd* dx = ws<cd>(W_X, (size_t)P * n);
+  double* dres = ws<double>(W_RESID, P);
+  double* dcond = ws<double>(W_COND, P);
+  int8_t* dreg = ws<int8_t>(W_REG, P);
+  int* drank = ws<int>(W_I32, P);
+  int8_t* dcls = ws<int8_t>(W_I8, P);
+  cd* sc = ws<cd>(W_SCR, (size_t)groups_of(blocks, n) * (3 * n * n + 2 * n));
+  if (!dx || !dres || !dcond || !dreg || !drank || !dcls || !sc) FAIL("out of device memory");
+  CK(cudaMemcpy(dx, x, (size_t)P * n * sizeof(cd), cudaMemcpyHostToDevice));
+  RefineArgs R;
+  R.H = h->dev();
+  R.P = P;
+  R.tol = tol;
+  R.iters = iters;
+  R.n_original = n_original;
+  R.inf_thr = infinity_threshold;
+  R.x = dx;
+  R.resid = dres;
+  R.cond = dcond;
+  R.regular = dreg;
+  R.rank = drank;
+  R.slack = dcls;
+  R.cscratch = sc;
+  k_refine[n](R, blocks, 0);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(x, dx, (size_t)P * n * sizeof(cd), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(residual, dres, P * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(condition, dcond, P * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(regular, dreg, P, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(rank, drank, P * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(slack_class, dcls, P, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int nid_dd_refine_batch(NidHomotopy* h, int P, double* x, int steps, int8_t* ok) {
+  if (!h || !x || !ok) FAIL("null argument");
+  if (h->nparam > 0) FAIL("dd refine does not take per-path parameters");
+  if (P <= 0) return 0;
+  const int n = h->n;
+  int blocks = grid_for(P, n, 4);
+  cd* dx = ws<cd>(W_X, (size_t)P * n);
+  int8_t* dok = ws<int8_t>(W_I8B, P);
+  cdd* sc = ws<cdd>(W_DDSCR, (size_t)groups_of(blocks, n) * (2 * n * n + 4 * n));
+  if (!dx || !dok || !sc) FAIL("out of device memory");
+  CK(cudaMemcpy(dx, x, (size_t)P * n * sizeof(cd), cudaMemcpyHostToDevice));
+  DDRefineArgs D;
+  D.H = h->dev();
+  D.P = P;
+  D.steps = steps;
+  D.x = dx;
+  D.ok = dok;
+  D.ddscratch = sc;
+  k_ddrefine[n](D, blocks, 0);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(x, dx, (size_t)P * n * sizeof(cd), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ok, dok, P, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int nid_match_pairs(int n, int ncmp, int P, const double* X, int32_t* pairs, long long max_pairs,
+                    long long* npairs) {
+  if (!X || !npairs) FAIL("null argument");
+  if (ncmp < 1 || ncmp > n) FAIL("need 1 <= ncmp <= n");
+  *npairs = 0;
+  if (P <= 1) return 0;
+  cd* dX = ws<cd>(W_X, (size_t)P * n);
+  double* tol = ws<double>(W_T, P);
+  int* dp = ws<int>(W_I32, (size_t)2 * (max_pairs > 0 ? max_pairs : 1));
+  unsigned long long* cnt = ws<unsigned long long>(W_COUNT, 8);
+  if (!dX || !tol || !dp || !cnt) FAIL("out of device memory");
+  CK(cudaMemcpy(dX, X, (size_t)P * n * sizeof(cd), cudaMemcpyHostToDevice));
+  CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
+  match_tol_kernel<<<(P + 255) / 256, 256>>>(n, ncmp, P, dX, tol);
+  match_pairs_kernel<<<(P + 127) / 128, 128>>>(n, ncmp, P, dX, tol, dp, max_pairs, cnt);
+  CK(cudaGetLastError());
+  unsigned long long c = 0;
+  CK(cudaMemcpy(&c, cnt, sizeof(c), cudaMemcpyDeviceToHost));
+  *npairs = (long long)c;
+  long long k = (long long)c < max_pairs ? (long long)c : max_pairs;
+  if (k > 0 && pairs) CK(cudaMemcpy(pairs, dp, (size_t)k * 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Explicit instantiation of every per-size kernel for one n = NID_N.
+// The build compiles this file once per n in 1..16 (in parallel), so each
+// size gets fully unrolled register-resident code.
+#include "endpoint.cuh"
+#include "launch.h"
+#include "track.cuh"
+
+#ifndef NID_N
+#error "NID_N must be defined"
+#endif
+
+namespace nid {
+
+static int blocks_for(const void* fn, int threads, int smem = 0) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
+  if (per < 1) per = 1;
+  return sms * per;
+}
+
+#define CAT_(a, b) a##b
+#define CAT(a, b) CAT_(a, b)
+
+int CAT(launch_track_, NID_N)(const TrackArgs& a, int max_blocks, cudaStream_t s) {
+  const void* fn = (const void*)track_kernel<NID_N>;
+  int blocks = blocks_for(fn, 128);
+  long long groups_per_block = 4 * (32 / NID_N);
+  long long need = (a.P + groups_per_block - 1) / groups_per_block;
+  if (need < blocks) blocks = (int)need;
+  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
+  if (blocks < 1) blocks = 1;
+  track_kernel<NID_N><<<blocks, 128, 0, s>>>(a);
+  return blocks;
+}
+
+int CAT(launch_endpoint_, NID_N)(const EndpointArgs& a, int blocks, cudaStream_t s) {
+  endpoint_kernel<NID_N><<<blocks, 128, 0, s>>>(a);
+  return blocks;
+}
+
+int CAT(launch_refine_, NID_N)(const RefineArgs& a, int blocks, cudaStream_t s) {
+  refine_kernel<NID_N><<<blocks, 128, 0, s>>>(a);
+  return blocks;
+}
+
+int CAT(launch_ddrefine_, NID_N)(const DDRefineArgs& a, int blocks, cudaStream_t s) {
+  ddrefine_kernel<NID_N><<<blocks, 128, 0, s>>>(a);
+  return blocks;
+}
+
+int CAT(launch_eval_, NID_N)(const EvalArgs& a, int blocks, cudaStream_t s) {
+  eval_kernel<NID_N><<<blocks, 128, 0, s>>>(a);
+  return blocks;
+}
+
+int CAT(launch_newton_, NID_N)(const NewtonArgs& a, int blocks, cudaStream_t s) {
+  newton_kernel<NID_N><<<blocks, 128, 0, s>>>(a);
+  return blocks;
+}
+
+int CAT(track_regs_, NID_N)() {
+  cudaFuncAttributes at;
+  if (cudaFuncGetAttributes(&at, (const void*)track_kernel<NID_N>) != cudaSuccess) return -1;
+  return at.numRegs;
+}
+
+}  // namespace nid

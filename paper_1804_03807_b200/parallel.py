@@ -1,0 +1,130 @@
+"""Multi-GPU plumbing: one process per GPU, paths sharded into equal
+contiguous ranges of the path index space, finite endpoints gathered to
+rank 0 for classification.
+
+The reference's only parallelism is the single-host work crew
+(parallel.py:69-137); paths are independent, so the data path has no
+collective.  The single exchange per stage is the endpoint gather (NCCL on
+GPUs, gloo in the CPU tests).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Equal contiguous shards; the first total % world ranks get one more."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(int(total), world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+@dataclass
+class DistContext:
+    rank: int = 0
+    world: int = 1
+    local_rank: int = 0
+    initialized_here: bool = False
+
+    @classmethod
+    def from_env(cls, expect_world: int | None = None, backend: str | None = None) -> "DistContext":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", str(rank)))
+        if expect_world is not None and world not in (1, expect_world):
+            raise ValueError(f"WORLD_SIZE={world} but --gpus {expect_world}")
+        ctx = cls(rank, world, local)
+        if world > 1:
+            import torch.distributed as dist
+
+            if not dist.is_initialized():
+                if backend is None:
+                    import torch
+
+                    backend = "nccl" if torch.cuda.is_available() else "gloo"
+                if backend == "nccl":
+                    import torch
+
+                    torch.cuda.set_device(local)
+                dist.init_process_group(backend=backend)
+                ctx.initialized_here = True
+        return ctx
+
+    def shard(self, total: int) -> tuple[int, int]:
+        return shard_range(total, self.rank, self.world)
+
+    def _device(self):
+        import torch
+        import torch.distributed as dist
+
+        if dist.get_backend() == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device("cpu")
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def max_over_ranks(self, v: float) -> float:
+        if self.world == 1:
+            return float(v)
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([float(v)], dtype=torch.float64, device=self._device())
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(self, v) -> int:
+        if self.world == 1:
+            return int(v)
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([int(v)], dtype=torch.int64, device=self._device())
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return int(t.item())
+
+    def close(self):
+        if self.initialized_here:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+def gather_finite(ctx: DistContext, x_end, status):
+    """Compact this rank's succeeded endpoints (status converged/singular)
+    and gather them to rank 0: all_gather of counts, then an all_gather of
+    the padded blocks (NCCL has no variable-size gather).  Returns the
+    concatenated [F, n, 2] tensor on rank 0, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    mask = (status == 0) | (status == 2)
+    pts = x_end[mask]
+    if ctx.world == 1:
+        return pts
+    cnt = torch.tensor([pts.shape[0]], dtype=torch.int64, device=pts.device)
+    counts = [torch.zeros_like(cnt) for _ in range(ctx.world)]
+    dist.all_gather(counts, cnt)
+    counts = [int(c.item()) for c in counts]
+    mx = max(counts)
+    pad = torch.zeros((mx,) + tuple(pts.shape[1:]), dtype=pts.dtype, device=pts.device)
+    pad[: pts.shape[0]] = pts
+    blocks = [torch.empty_like(pad) for _ in range(ctx.world)]
+    dist.all_gather(blocks, pad)
+    if ctx.rank != 0:
+        return None
+    return torch.cat([b[:c] for b, c in zip(blocks, counts)], dim=0)
+
+
+def merge_shards(parts: list[np.ndarray]) -> np.ndarray:
+    return np.concatenate(parts, axis=0) if parts else np.zeros((0,))

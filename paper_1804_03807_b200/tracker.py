@@ -1,0 +1,285 @@
+"""Path tracking on the GPU behind the reference's tracker API.
+
+Mirrors `nidpipe.tracker` (pkg/src/nidpipe/tracker.py): the status and
+slack constants (:33-46), `Solution` (:137-154), `PathResult` (:157-166),
+`track` (:341-407), `newton_refine` (:410-428), `refine_dd` (:431-435),
+`classify` (:438-455), plus `newton_step` / `condition_and_rank`
+(linalg.py:13-51).  Every numeric call goes through libnid.so; there is no
+CPU path.  `track_batch` is the batched entry point the drivers use: it is
+the GPU replacement of `work_crew(jobs, p, lambda x0: track(h, x0, params))`
+(cascade.py:230,312, filtering.py:115).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .homotopy import DeviceHomotopy, LinearHomotopy, TrackParams, lower, system_homotopy  # noqa: F401
+from .polys import PolySystem
+
+REGULAR = "regular"
+SINGULAR = "singular"
+CONVERGED = "converged"
+AT_INFINITY = "at_infinity"
+SINGULAR_ENDPOINT = "singular_endpoint"
+FAILED = "failed"
+ZERO_SLACK = "zero_slack"
+NONZERO_SLACK = "nonzero_slack"
+NOT_APPLICABLE = "not_applicable"
+ZERO_SLACK_TOL = 1e-8
+CONVERGED_RESIDUAL = 1e-8
+SINGULARITY_TOL = 1e-8
+
+STATUS_NAMES = (CONVERGED, AT_INFINITY, SINGULAR_ENDPOINT, FAILED)
+STATUS_CODES = {s: i for i, s in enumerate(STATUS_NAMES)}
+SLACK_NAMES = {_lib.CLS_AT_INFINITY: AT_INFINITY, _lib.CLS_ZERO: ZERO_SLACK, _lib.CLS_NONZERO: NONZERO_SLACK}
+
+
+@dataclass(frozen=True)
+class Solution:
+    coordinates: np.ndarray
+    residual: float
+    condition: float
+    regularity: str = REGULAR
+    slack_class: str = NOT_APPLICABLE
+
+    def __post_init__(self):
+        object.__setattr__(self, "coordinates", np.asarray(self.coordinates, dtype=np.complex128))
+
+    @property
+    def is_regular(self) -> bool:
+        return self.regularity == REGULAR
+
+
+@dataclass(frozen=True)
+class PathResult:
+    status: str
+    endpoint: Solution | None
+    steps_used: int
+    t_reached: float
+
+    @property
+    def succeeded(self) -> bool:
+        return self.status in (CONVERGED, SINGULAR_ENDPOINT)
+
+
+@dataclass
+class TrackResults:
+    """Struct-of-arrays results of one batched launch, in job order."""
+
+    x: np.ndarray  # [P, n] endpoint coordinates (NaN where none)
+    status: np.ndarray  # int8 codes (STATUS_NAMES)
+    steps: np.ndarray
+    t_reached: np.ndarray
+    residual: np.ndarray
+    condition: np.ndarray
+    regular: np.ndarray  # 1 regular, 0 singular, -1 none
+    counters: dict
+
+    def __len__(self):
+        return int(self.status.size)
+
+    @property
+    def succeeded(self) -> np.ndarray:
+        return (self.status == 0) | (self.status == 2)
+
+    def counts(self) -> dict:
+        return {name: int(np.sum(self.status == i)) for i, name in enumerate(STATUS_NAMES)}
+
+    def result(self, i: int) -> PathResult:
+        st = STATUS_NAMES[int(self.status[i])]
+        ep = None
+        if st in (CONVERGED, SINGULAR_ENDPOINT):
+            ep = Solution(self.x[i].copy(), float(self.residual[i]), float(self.condition[i]),
+                          REGULAR if self.regular[i] == 1 else SINGULAR)
+        return PathResult(st, ep, int(self.steps[i]), float(self.t_reached[i]))
+
+    def path_results(self) -> list[PathResult]:
+        return [self.result(i) for i in range(len(self))]
+
+
+def _device_of(h) -> DeviceHomotopy:
+    if isinstance(h, DeviceHomotopy):
+        return h
+    if isinstance(h, LinearHomotopy):
+        return h.device()
+    raise TypeError("expected a LinearHomotopy (the GPU path tracks lowered linear homotopies)")
+
+
+def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=None, first_index: int = 0,
+                count: int | None = None, target_params=None, param_div: int = 1,
+                out: TrackResults | None = None) -> TrackResults:
+    """Track many paths of h in one launch.
+
+    starts: [P, n] start points, or None with `degrees` for total-degree
+    starts generated on the device for path indices [first_index, first_index+count).
+    target_params: per-path target coefficients ([P/param_div, nparam]) for
+    homotopies lowered with parameter slots (membership tests)."""
+    L = _lib.lib()
+    dev = _device_of(h)
+    n = dev.n
+    if starts is not None:
+        st = np.ascontiguousarray(starts, dtype=np.complex128).reshape(-1, n)
+        P = st.shape[0]
+        deg = None
+    else:
+        if degrees is None or count is None:
+            raise ValueError("give start points, or degrees and count for total-degree starts")
+        st = None
+        P = int(count)
+        deg = np.ascontiguousarray(degrees, dtype=np.int32)
+    prm = None if target_params is None else np.ascontiguousarray(target_params, dtype=np.complex128)
+    if out is None:  # (callers may pass preallocated, e.g. pinned, host arrays)
+        out = TrackResults(np.empty((P, n), np.complex128), np.empty(P, np.int8), np.empty(P, np.int32),
+                           np.empty(P, np.float64), np.empty(P, np.float64), np.empty(P, np.float64),
+                           np.empty(P, np.int8), {})
+    o = _lib.PathOutC(_lib.ptr(out.x), _lib.ptr(out.status), _lib.ptr(out.steps), _lib.ptr(out.t_reached),
+                      _lib.ptr(out.residual), _lib.ptr(out.condition), _lib.ptr(out.regular))
+    pc = params.to_c()
+    _lib.check(L.nid_track_batch(dev.handle, C.byref(pc), P, _lib.ptr(st), int(first_index), _lib.ptr(deg),
+                                 _lib.ptr(prm), int(param_div), C.byref(o), 0, None), L)
+    out.counters = _lib.last_counters()
+    return out
+
+
+def track(h, x0, params: TrackParams = TrackParams(), trace: list | None = None) -> PathResult:
+    """Track one path (tracker.py:341-407) -- a batch of one on the GPU."""
+    if trace is not None:
+        raise NotImplementedError("per-step traces are not recorded by the GPU tracker")
+    return track_batch(h, np.asarray(x0, dtype=np.complex128)[None], params).result(0)
+
+
+def newton_step(J, r):
+    """Solve J dx = -r (zgesv; min-norm lstsq fallback) on the GPU (linalg.py:35-51)."""
+    J = np.ascontiguousarray(J, dtype=np.complex128)
+    r = np.ascontiguousarray(r, dtype=np.complex128)
+    single = J.ndim == 2
+    if single:
+        J, r = J[None], r[None]
+    P, n, m = J.shape
+    if n != m:
+        raise ValueError("newton_step on the GPU needs square Jacobians")
+    dx = np.empty((P, n), np.complex128)
+    L = _lib.lib()
+    _lib.check(L.nid_newton_step_batch(n, P, _lib.ptr(J), _lib.ptr(r), _lib.ptr(dx)), L)
+    return dx[0] if single else dx
+
+
+def singular_values(A) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    single = A.ndim == 2
+    if single:
+        A = A[None]
+    P, m, n = A.shape
+    if m < n:
+        A = np.ascontiguousarray(np.conj(np.swapaxes(A, 1, 2)))
+        P, m, n = A.shape
+    sv = np.empty((P, n), np.float64)
+    L = _lib.lib()
+    _lib.check(L.nid_svd_batch(m, n, P, _lib.ptr(A), _lib.ptr(sv)), L)
+    return sv[0] if single else sv
+
+
+def condition_and_rank(J, tol: float = SINGULARITY_TOL):
+    """linalg.py:13-32, singular values from the GPU Jacobi SVD."""
+    J = np.asarray(J, dtype=np.complex128)
+    if J.size == 0:
+        raise ValueError("empty matrix")
+    if not np.all(np.isfinite(J.view(np.float64))):
+        return float("inf"), 0
+    s = singular_values(J)
+    smax = float(s[0])
+    if smax == 0.0:
+        return float("inf"), 0
+    rank = int(np.sum(s > tol * smax))
+    smin = float(s[min(J.shape) - 1])
+    return (float("inf") if smin == 0.0 else smax / smin), rank
+
+
+@dataclass
+class RefineResults:
+    x: np.ndarray
+    residual: np.ndarray
+    condition: np.ndarray
+    regular: np.ndarray
+    rank: np.ndarray
+    slack: np.ndarray  # slack class codes
+
+    def solution(self, i, with_slack=False) -> Solution:
+        return Solution(self.x[i].copy(), float(self.residual[i]), float(self.condition[i]),
+                        REGULAR if self.regular[i] else SINGULAR,
+                        SLACK_NAMES[int(self.slack[i])] if with_slack else NOT_APPLICABLE)
+
+
+def refine_batch(f: PolySystem, X, tol: float = 1e-12, max_iters: int = 10, n_original: int | None = None,
+                 infinity_threshold: float = 1e8, h: LinearHomotopy | None = None) -> RefineResults:
+    """newton_refine + classify for many points in one launch."""
+    h = h or system_homotopy(f)
+    dev = h.device()
+    n = dev.n
+    X = np.array(X, dtype=np.complex128).reshape(-1, n)
+    P = X.shape[0]
+    res = RefineResults(X, np.empty(P), np.empty(P), np.empty(P, np.int8), np.empty(P, np.int32),
+                        np.empty(P, np.int8))
+    if P == 0:
+        return res
+    L = _lib.lib()
+    _lib.check(L.nid_refine_batch(dev.handle, P, _lib.ptr(X), float(tol), int(max_iters),
+                                  int(n if n_original is None else n_original), float(infinity_threshold),
+                                  _lib.ptr(res.residual), _lib.ptr(res.condition), _lib.ptr(res.regular),
+                                  _lib.ptr(res.rank), _lib.ptr(res.slack)), L)
+    return res
+
+
+def newton_refine(f: PolySystem, x, tol: float = 1e-12, max_iters: int = 10) -> Solution:
+    """tracker.py:410-428"""
+    return refine_batch(f, np.asarray(x, dtype=np.complex128)[None], tol, max_iters).solution(0)
+
+
+def refine_dd_batch(f: PolySystem, X, steps: int = 3, h: LinearHomotopy | None = None):
+    h = h or system_homotopy(f)
+    dev = h.device()
+    X = np.array(X, dtype=np.complex128).reshape(-1, dev.n)
+    ok = np.empty(X.shape[0], np.int8)
+    if X.shape[0]:
+        L = _lib.lib()
+        _lib.check(L.nid_dd_refine_batch(dev.handle, X.shape[0], _lib.ptr(X), int(steps), _lib.ptr(ok)), L)
+    return X, ok
+
+
+def refine_dd(f: PolySystem, x, steps: int = 3) -> np.ndarray:
+    """tracker.py:431-435"""
+    return refine_dd_batch(f, np.asarray(x, dtype=np.complex128)[None], steps)[0][0]
+
+
+def classify(coords, n_original: int, infinity_threshold: float = 1e8, zero_tol: float = ZERO_SLACK_TOL) -> str:
+    """Three-way slack classification (tracker.py:438-455); pure bookkeeping."""
+    c = np.asarray(coords, dtype=np.complex128)
+    if not np.all(np.isfinite(c.view(np.float64))) or float(np.max(np.abs(c))) > infinity_threshold:
+        return AT_INFINITY
+    s = c[n_original:]
+    if s.size == 0 or float(np.max(np.abs(s))) < zero_tol:
+        return ZERO_SLACK
+    return NONZERO_SLACK
+
+
+def track_batch_device(h, params: TrackParams, P: int, out: dict, *, degrees=None, first_index: int = 0,
+                       starts_ptr: int = 0, params_ptr: int = 0, param_div: int = 1, stream: int = 0) -> dict:
+    """Device-resident variant of `track_batch`: every buffer is a device
+    pointer (e.g. torch CUDA tensors' data_ptr()), nothing is copied, and the
+    kernels run on `stream`.  `out` maps x_end/status/steps/t_reached/
+    residual/condition/regular to device pointers."""
+    L = _lib.lib()
+    dev = _device_of(h)
+    deg = None if degrees is None else np.ascontiguousarray(degrees, dtype=np.int32)
+    o = _lib.PathOutC(out["x_end"], out["status"], out["steps"], out["t_reached"], out["residual"],
+                      out["condition"], out["regular"])
+    pc = params.to_c()
+    _lib.check(L.nid_track_batch(dev.handle, C.byref(pc), int(P), C.c_void_p(starts_ptr or None),
+                                 int(first_index), _lib.ptr(deg), C.c_void_p(params_ptr or None), int(param_div),
+                                 C.byref(o), 1, C.c_void_p(stream or None)), L)
+    return _lib.last_counters()
