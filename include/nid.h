@@ -21,7 +21,6 @@
  *   nid_refine_batch      newton_refine + classify                     tracker.py:410-455
  *   nid_dd_refine_batch   refine_dd                                    tracker.py:431-435
  *   nid_match_pairs       points_match over all pairs (for _dedup)     filtering.py:73-78,140-150
- *   nid_match_candidates  membership verdict reduction                 filtering.py:115-127
  */
 #ifndef NID_H
 #define NID_H
@@ -77,6 +76,11 @@ typedef struct NidHomotopyDesc {
   const int8_t* param_slot; /* [nterms] or NULL */
   int32_t nparam;
   double gamma_re, gamma_im;
+  /* start_kind 1: the start system is total degree, G_i = x_i^{d_i} - 1 with
+   * d_i = start_degrees[i]; it is evaluated in closed form and the term
+   * table then carries only the target system (coef_start all zero). */
+  int32_t start_kind;
+  const int32_t* start_degrees;
 } NidHomotopyDesc;
 
 typedef struct NidHomotopy NidHomotopy;

@@ -10,6 +10,7 @@
 #include "endpoint.cuh"
 #include "launch.h"
 #include "track.cuh"
+#include "track_ctl.cuh"
 
 static thread_local std::string g_err;
 static NidCounters g_counters = {};
@@ -30,7 +31,8 @@ static int g_device = -1;
   } while (0)
 
 struct NidHomotopy {
-  int n, nterms, nparam, maxdeg;
+  int n, nterms, nparam, maxdeg, multilinear, td;
+  int tddeg[NID_MAX_VARS];
   cd gamma;
   int* row_off;
   uint4* expo;
@@ -43,6 +45,9 @@ struct NidHomotopy {
     h.nterms = nterms;
     h.nparam = nparam;
     h.maxdeg = maxdeg;
+    h.multilinear = multilinear;
+    h.td = td;
+    for (int v = 0; v < NID_MAX_VARS; ++v) h.tddeg[v] = tddeg[v];
     h.row_off = row_off;
     h.expo = expo;
     h.cs = cs;
@@ -94,6 +99,7 @@ static const DDRefineFn k_ddrefine[17] = NID_TABLE(launch_ddrefine_);
 static const EvalFn k_eval[17] = NID_TABLE(launch_eval_);
 static const NewtonFn k_newton[17] = NID_TABLE(launch_newton_);
 static const RegsFn k_regs[17] = NID_TABLE(track_regs_);
+static const RegsFn k_tthreads[17] = NID_TABLE(track_threads_);
 
 static int sm_count() {
   int dev = 0, sms = 148;
@@ -163,11 +169,22 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
       if (a > maxdeg) maxdeg = a;
     }
   }
+  if (d->start_kind != 0 && d->start_kind != 1) FAIL("unknown start_kind");
+  if (d->start_kind == 1) {
+    if (!d->start_degrees) FAIL("total-degree start needs start_degrees");
+    for (int v = 0; v < n; ++v)
+      if (d->start_degrees[v] < 1) FAIL("total-degree start degrees must be >= 1");
+    for (int k = 0; k < 2 * T; ++k)
+      if (d->coef_start[k] != 0.0) FAIL("total-degree start: the term table must hold only the target");
+  }
   NidHomotopy* h = new NidHomotopy();
   h->n = n;
   h->nterms = T;
   h->nparam = d->nparam;
   h->maxdeg = maxdeg;
+  h->multilinear = maxdeg <= 1 ? 1 : 0;
+  h->td = d->start_kind == 1 ? 1 : 0;
+  for (int v = 0; v < NID_MAX_VARS; ++v) h->tddeg[v] = (h->td && v < n) ? d->start_degrees[v] : 0;
   h->gamma = cd{d->gamma_re, d->gamma_im};
   const size_t Tp = T > 0 ? T : 1;
   cudaError_t e = cudaSuccess;
@@ -217,7 +234,7 @@ int nid_last_counters(NidCounters* c) {
 // slot map for the workspace cache
 enum {
   W_STARTS = 0, W_PARAMS, W_XEND, W_STATUS, W_STEPS, W_TREACH, W_RESID, W_COND, W_REG,
-  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL
+  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS
 };
 
 int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
@@ -284,9 +301,24 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
   a.first_index = first_index;
   a.starts = d_starts;
   for (int v = 0; v < NID_MAX_VARS; ++v) a.deg[v] = (degrees && v < n) ? degrees[v] : 1;
-  if (!starts)
-    for (int v = 0; v < n; ++v)
+  if (!starts) {
+    // roots of unity exp(2 pi i k/d) = cos/sin(pi * (2k/d)), the formula of
+    // systems.total_degree_starts on the host side
+    std::vector<cd> roots;
+    for (int v = 0; v < n; ++v) {
       if (a.deg[v] < 1) FAIL("total-degree start degrees must be >= 1");
+      a.root_off[v] = (int)roots.size();
+      for (int k = 0; k < a.deg[v]; ++k) {
+        double ang = 3.141592653589793 * (2.0 * (double)k / (double)a.deg[v]);
+        roots.push_back(cd{cos(ang), sin(ang)});
+      }
+    }
+    cd* dr = ws<cd>(W_ROOTS, roots.size());
+    if (!dr) FAIL("out of device memory (roots)");
+    CK(cudaMemcpyAsync(dr, roots.data(), roots.size() * sizeof(cd), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    a.roots = dr;
+  }
   a.params = d_params;
   a.param_div = param_div;
   a.next = d_cnt + 7;
@@ -296,9 +328,9 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
   a.t_reached = d_tr;
   a.resid = d_res;
   a.counters = d_cnt;
-  // lstsq scratch for every resident group
+  // lstsq scratch for every resident thread (one path per thread)
   const int max_blocks = sm_count() * 8;
-  a.scratch = ws<cd>(W_SCR, (size_t)groups_of(max_blocks, n) * (3 * n * n + 2 * n));
+  a.scratch = ws<cd>(W_SCR, (size_t)max_blocks * k_tthreads[n]() * (3 * n * n + 2 * n));
   if (!a.scratch) FAIL("out of device memory (scratch)");
 
   cudaEvent_t e0, e1, e2;

@@ -294,10 +294,9 @@ template <int N>
 NID_D void group_newton_step(const Grp<N>& g, const HomDev& H, const cd (&x)[N], const cd* prm, cd (&J)[N],
                              cd hv, cd* sc, cd (&dx)[N]) {
   cd mine;
-  cd Jc[N];
 #pragma unroll
-  for (int v = 0; v < N; ++v) Jc[v] = J[v];
-  bool ok = group_lu_solve<N>(g, Jc, -hv, dx, mine);
+  for (int v = 0; v < N; ++v) dx[v] = J[v];
+  bool ok = group_lu_solve<N>(g, dx, -hv, mine);
   if (!ok) {
 #pragma unroll
     for (int v = 0; v < N; ++v) sc[g.lg * N + v] = J[v];
@@ -476,17 +475,14 @@ __global__ void __launch_bounds__(128) newton_kernel(NewtonArgs A) {
   const long long ngroups = (long long)gridDim.x * blockDim.x / 32 * (32 / N);
   cd* sc = A.cscratch + gslot * (3 * N * N + 2 * N);
   for (long long p = gslot; p < A.P; p += ngroups) {
-    cd Jr[N], dx[N], mine;
+    cd dx[N], mine;
 #pragma unroll
-    for (int v = 0; v < N; ++v) Jr[v] = A.J[(p * N + g.lg) * N + v];
+    for (int v = 0; v < N; ++v) dx[v] = A.J[(p * N + g.lg) * N + v];
     cd rr = A.r[p * N + g.lg];
-    cd Jc[N];
-#pragma unroll
-    for (int v = 0; v < N; ++v) Jc[v] = Jr[v];
-    bool ok = group_lu_solve<N>(g, Jc, -rr, dx, mine);
+    bool ok = group_lu_solve<N>(g, dx, -rr, mine);
     if (!ok) {
 #pragma unroll
-      for (int v = 0; v < N; ++v) sc[g.lg * N + v] = Jr[v];
+      for (int v = 0; v < N; ++v) sc[g.lg * N + v] = A.J[(p * N + g.lg) * N + v];
       sc[N * N + g.lg] = -rr;
       __syncwarp(g.mask);
       if (g.lg == 0) {

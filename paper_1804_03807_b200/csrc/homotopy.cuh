@@ -4,18 +4,28 @@
 // stacked evaluator underneath (polynomials.py:202-256, eval_magnitude
 // :282-287).  Start and target rows are merged into one term table; a term
 // contributes c(t) * x^a with c(t) = (1-t) gamma c_start + t c_target, so
-// rows shared by both systems cost one monomial pass instead of two.
+// rows shared by both systems cost one monomial pass instead of two.  A
+// total-degree start system G_i = x_i^{d_i} - 1 is not stored as terms: lane
+// i evaluates it in closed form.
 //
 // Lane i of a path group owns row i: it forms each term's monomial and all
 // of its partial derivatives from one prefix pass and one suffix pass over
 // the exponent vector (shared factors: the leave-one-out product of every
 // variable), accumulating H_i and the full Jacobian row i in registers.
+// The per-variable work is branch-free (selects, not branches): lanes of a
+// warp evaluate different rows with different exponent patterns and must
+// not diverge.  Tables whose exponents are all 0/1 (multilinear, e.g. the
+// cyclic systems) take a cheaper path; otherwise powers up to the table's
+// maximum degree are formed with predicated products.
 // The point x is held, complete, by every lane of the group.
 #pragma once
 #include "nid_common.cuh"
 
 struct HomDev {
   int n, nterms, nparam, maxdeg;
+  int multilinear;        // every table exponent is 0 or 1
+  int td;                 // start system is total degree (closed form)
+  int tddeg[NID_MAX_VARS];
   const int* row_off;     // [n+1]
   const uint4* expo;      // [nterms], 16 exponent bytes
   const cd* cs;           // start coefficients
@@ -33,10 +43,28 @@ NID_D cd ldg_c(const cd* p) {
 
 NID_D int expo_at(const unsigned (&w)[4], int v) { return (w[v >> 2] >> (8 * (v & 3))) & 0xff; }
 
-NID_D cd cpow_small(cd x, int a) {  // x^a, a >= 1, by repeated products like the reference's power table
-  cd r = x;
-  for (int e = 1; e < a; ++e) r = r * x;
-  return r;
+NID_D cd csel(bool c, cd a, cd b) { return cd{c ? a.re : b.re, c ? a.im : b.im}; }
+
+// x^a and a*x^(a-1) for 0 <= a <= maxdeg, branch-free across lanes
+// (repeated products like the reference's power table)
+NID_D void cpow_pair(cd x, int a, int maxdeg, cd& f, cd& d) {
+  cd pw = x, prev = cd{1.0, 0.0};
+#pragma unroll 1
+  for (int e = 2; e <= maxdeg; ++e) {
+    const bool m = e <= a;
+    const cd nx = pw * x;
+    prev = csel(m, pw, prev);
+    pw = csel(m, nx, pw);
+  }
+  f = csel(a > 0, pw, cd{1.0, 0.0});
+  d = csel(a > 0, (double)a * prev, cd{0.0, 0.0});
+}
+
+NID_D double rpow_small(double x, int a, int maxdeg) {
+  double p = 1.0;
+#pragma unroll 1
+  for (int e = 1; e <= maxdeg; ++e) p = (e <= a) ? __dmul_rn(p, x) : p;
+  return p;
 }
 
 // Row `row` of H(x, t), its Jacobian row, and the start/target abs sums
@@ -55,39 +83,72 @@ NID_D void eval_row(const HomDev& H, int row, const cd (&x)[N], double t, const 
     k0 = __ldg(H.row_off + row);
     k1 = __ldg(H.row_off + row + 1);
   }
+  const bool ml = H.multilinear != 0;
+  const int maxdeg = H.maxdeg;
   for (int k = k0; k < k1; ++k) {
     uint4 ew = __ldg(H.expo + k);
     const unsigned w[4] = {ew.x, ew.y, ew.z, ew.w};
-    cd cs = ldg_c(H.cs + k), ct = ldg_c(H.ct + k);
+    cd ct = ldg_c(H.ct + k);
     if (H.pslot != nullptr) {
       int s = H.pslot[k];
       if (s >= 0) ct = prm[s];
     }
-    const cd c = alpha * cs + t * ct;
-    // prefix products P[v] = prod_{u<v} x_u^{a_u}
+    const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
     cd P[N];
     cd p = cd{1.0, 0.0};
+    if (ml) {
+      // prefix products P[v] = prod_{u<v} x_u^{a_u}
 #pragma unroll
-    for (int v = 0; v < N; ++v) {
-      P[v] = p;
-      int a = expo_at(w, v);
-      if (a == 1) p = p * x[v];
-      else if (a > 1) p = p * cpow_small(x[v], a);
-    }
-    hv = cfma(c, p, hv);
-    // suffix sweep: d/dx_v = a_v x_v^{a_v-1} * P[v] * S[v]
-    cd s = cd{1.0, 0.0};
-#pragma unroll
-    for (int v = N - 1; v >= 0; --v) {
-      int a = expo_at(w, v);
-      if (a == 1) {
-        J[v] = cfma(P[v] * s, c, J[v]);
-        s = s * x[v];
-      } else if (a > 1) {
-        cd q = cpow_small(x[v], a - 1);
-        J[v] = cfma(P[v] * s, (double)a * (c * q), J[v]);
-        s = s * (q * x[v]);
+      for (int v = 0; v < N; ++v) {
+        P[v] = p;
+        p = csel(expo_at(w, v) != 0, p * x[v], p);
       }
+      hv = cfma(c, p, hv);
+      // suffix sweep: d/dx_v = P[v] * S[v]
+      cd s = cd{1.0, 0.0};
+#pragma unroll
+      for (int v = N - 1; v >= 0; --v) {
+        const bool on = expo_at(w, v) != 0;
+        J[v] = csel(on, cfma(P[v] * s, c, J[v]), J[v]);
+        s = csel(on, s * x[v], s);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < N; ++v) {
+        P[v] = p;
+        cd f, d;
+        cpow_pair(x[v], expo_at(w, v), maxdeg, f, d);
+        p = p * f;
+      }
+      hv = cfma(c, p, hv);
+      cd s = cd{1.0, 0.0};
+#pragma unroll
+      for (int v = N - 1; v >= 0; --v) {
+        const int a = expo_at(w, v);
+        cd f, d;
+        cpow_pair(x[v], a, maxdeg, f, d);
+        J[v] = csel(a != 0, cfma(P[v] * s, c * d, J[v]), J[v]);
+        s = s * f;
+      }
+    }
+  }
+  // total-degree start row: G_i = x_i^{d_i} - 1, dG_i/dx_i = d_i x_i^{d_i - 1}
+  double xa_td = 0.0;
+  if (H.td && row < H.n) {
+    const int d = H.tddeg[row];
+    const cd xi = pick<N>(x, row);
+    cd q = cd{1.0, 0.0};
+    for (int e = 1; e < d; ++e) q = q * xi;
+    const cd f = q * xi;
+    hv = cfma(alpha, f - cd{1.0, 0.0}, hv);
+    const cd dj = alpha * ((double)d * q);
+#pragma unroll
+    for (int v = 0; v < N; ++v) J[v] = csel(v == row, J[v] + dj, J[v]);
+    if (want_scale) {
+      const double ax = cabsd(xi);
+      double m = 1.0;
+      for (int e = 0; e < d; ++e) m = __dmul_rn(m, ax);
+      xa_td = m;
     }
   }
   if (want_scale) {
@@ -99,45 +160,21 @@ NID_D void eval_row(const HomDev& H, int row, const cd (&x)[N], double t, const 
       const unsigned w[4] = {ew.x, ew.y, ew.z, ew.w};
       double m = 1.0;
 #pragma unroll
-      for (int v = 0; v < N; ++v) {
-        int a = expo_at(w, v);
-        double pv = 1.0;
-        for (int e = 0; e < a; ++e) pv = __dmul_rn(pv, ax[v]);
-        m = __dmul_rn(m, pv);
-      }
-      sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
+      for (int v = 0; v < N; ++v) m = __dmul_rn(m, rpow_small(ax[v], expo_at(w, v), maxdeg));
+      if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
       sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), m));
     }
+    // |G_i| terms sorted as the reference stores them: constant, then x_i^d
+    if (H.td && row < H.n) sS = __dadd_rn(1.0, xa_td);
   }
 }
 
 // Value-only variant (no Jacobian), used where only residuals are needed.
 template <int N>
 NID_D cd eval_row_value(const HomDev& H, int row, const cd (&x)[N], double t, const cd* prm) {
-  const cd alpha = (1.0 - t) * H.gamma;
-  cd hv = cd{0.0, 0.0};
-  int k0 = 0, k1 = 0;
-  if (row < H.n) {
-    k0 = __ldg(H.row_off + row);
-    k1 = __ldg(H.row_off + row + 1);
-  }
-  for (int k = k0; k < k1; ++k) {
-    uint4 ew = __ldg(H.expo + k);
-    const unsigned w[4] = {ew.x, ew.y, ew.z, ew.w};
-    cd cs = ldg_c(H.cs + k), ct = ldg_c(H.ct + k);
-    if (H.pslot != nullptr) {
-      int s = H.pslot[k];
-      if (s >= 0) ct = prm[s];
-    }
-    const cd c = alpha * cs + t * ct;
-    cd p = cd{1.0, 0.0};
-#pragma unroll
-    for (int v = 0; v < N; ++v) {
-      int a = expo_at(w, v);
-      if (a == 1) p = p * x[v];
-      else if (a > 1) p = p * cpow_small(x[v], a);
-    }
-    hv = cfma(c, p, hv);
-  }
+  cd J[N];
+  cd hv;
+  double sS, sT;
+  eval_row<N>(H, row, x, t, prm, hv, J, sS, sT, false);
   return hv;
 }

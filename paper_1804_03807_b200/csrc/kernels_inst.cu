@@ -4,6 +4,7 @@
 #include "endpoint.cuh"
 #include "launch.h"
 #include "track.cuh"
+#include "track_ctl.cuh"
 
 #ifndef NID_N
 #error "NID_N must be defined"
@@ -23,15 +24,18 @@ static int blocks_for(const void* fn, int threads, int smem = 0) {
 #define CAT_(a, b) a##b
 #define CAT(a, b) CAT_(a, b)
 
+// row-split thread-per-path tracker: 32 path slots per block, G warps
 int CAT(launch_track_, NID_N)(const TrackArgs& a, int max_blocks, cudaStream_t s) {
-  const void* fn = (const void*)track_kernel<NID_N>;
-  int blocks = blocks_for(fn, 128);
-  long long groups_per_block = 4 * (32 / NID_N);
-  long long need = (a.P + groups_per_block - 1) / groups_per_block;
+  const void* fn = (const void*)track_ctl_kernel<NID_N>;
+  const int threads = 32 * rows::groups<NID_N>();
+  const int smem = (int)ctl::Lay<NID_N>::bytes();
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int blocks = blocks_for(fn, threads, smem);
+  long long need = (a.P + rows::SLOTS - 1) / rows::SLOTS;
   if (need < blocks) blocks = (int)need;
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  track_kernel<NID_N><<<blocks, 128, 0, s>>>(a);
+  track_ctl_kernel<NID_N><<<blocks, threads, smem, s>>>(a);
   return blocks;
 }
 
@@ -62,8 +66,10 @@ int CAT(launch_newton_, NID_N)(const NewtonArgs& a, int blocks, cudaStream_t s) 
 
 int CAT(track_regs_, NID_N)() {
   cudaFuncAttributes at;
-  if (cudaFuncGetAttributes(&at, (const void*)track_kernel<NID_N>) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&at, (const void*)track_ctl_kernel<NID_N>) != cudaSuccess) return -1;
   return at.numRegs;
 }
+
+int CAT(track_threads_, NID_N)() { return rows::SLOTS; }  // path slots per block
 
 }  // namespace nid

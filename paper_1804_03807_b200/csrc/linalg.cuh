@@ -9,35 +9,38 @@
 #pragma once
 #include "nid_common.cuh"
 
-// Group LU solve of A x = b (elimination arithmetic unfused, as LAPACK's
-// zgetf2/zgetrs update loops round it, so exactly rank-deficient Jacobians
-// produce the same exact zero pivot and the same lstsq fallback); lane lg holds row lg of A and b[lg].  Rows are
-// never moved: the pivot row of step k is broadcast from its lane and the
-// permutation lives in pl[] (uniform across the group).  Pivot choice is
-// LAPACK's izamax rule: largest |Re|+|Im| in column k among the rows not yet
-// used, ties to the row that comes first in LAPACK's swapped order (`pos`).
-// Every lane ends with the full solution x[]; mine = x[lg].  Returns false
-// on an exactly zero pivot or a non-finite solution.
+// Group LU solve of A x = b, in place: lane lg holds row lg of A and b[lg];
+// on return every lane holds the full solution in A[0..N-1] and mine =
+// x[lg].  Rows are never moved: the pivot row of step k is broadcast from
+// its lane, and each lane remembers the step it pivoted (mystep); the
+// back substitution finds step k's lane by ballot.  Pivot choice is
+// LAPACK's izamax rule (largest |Re|+|Im| in column k among unused rows,
+// ties to the row first in LAPACK's swapped order, `pos`).  Elimination
+// arithmetic is unfused, as LAPACK's zgetf2/zgetrs update loops round it,
+// so exactly rank-deficient Jacobians produce the same exact zero pivot
+// (and the same lstsq fallback) as zgesv.  The k loops run at runtime
+// (uniform across the warp) to keep the kernel inside the instruction
+// cache.  Returns false on an exactly zero pivot or a non-finite solution.
 template <int N>
-NID_D bool group_lu_solve(const Grp<N>& g, cd (&A)[N], cd b, cd (&x)[N], cd& mine) {
+NID_D bool group_lu_solve(const Grp<N>& g, cd (&A)[N], cd b, cd& mine) {
   bool used = false;
   int pos = g.lg, mystep = N;
-  int pl[N];
   bool bad = false;
-#pragma unroll
+#pragma unroll 1
   for (int k = 0; k < N; ++k) {
-    double key = used ? -1.0 : cabs1(A[k]);
+    const cd ak = pick<N>(A, k);
+    double key = used ? -1.0 : cabs1(ak);
     if (isnan(key)) key = -0.5;
     double bk = key;
     int bp = pos, bl = g.lg;
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) {
       if (s < N) {
-        bool ok = (g.lg + s < N) && (g.lane + s < 32);
-        int src = ok ? g.lane + s : g.lane;
-        double ok_k = __shfl_sync(g.mask, bk, src);
-        int ok_p = __shfl_sync(g.mask, bp, src);
-        int ok_l = __shfl_sync(g.mask, bl, src);
+        const bool ok = (g.lg + s < N) && (g.lane + s < 32);
+        const int src = ok ? g.lane + s : g.lane;
+        const double ok_k = __shfl_sync(g.mask, bk, src);
+        const int ok_p = __shfl_sync(g.mask, bp, src);
+        const int ok_l = __shfl_sync(g.mask, bl, src);
         if (ok && (ok_k > bk || (ok_k == bk && ok_p < bp))) {
           bk = ok_k;
           bp = ok_p;
@@ -49,7 +52,6 @@ NID_D bool group_lu_solve(const Grp<N>& g, cd (&A)[N], cd b, cd (&x)[N], cd& min
     bp = __shfl_sync(g.mask, bp, g.gbase);
     bl = __shfl_sync(g.mask, bl, g.gbase);
     if (!(bk > 0.0)) bad = true;
-    pl[k] = bl;
     const bool me = (g.lg == bl);
     if (!me && pos == k) pos = bp;
     if (me) {
@@ -58,26 +60,33 @@ NID_D bool group_lu_solve(const Grp<N>& g, cd (&A)[N], cd b, cd (&x)[N], cd& min
       mystep = k;
     }
     const int src = g.src(bl);
-    const cd inv = crecip(shfl_c(g.mask, A[k], src));
-    const cd l = cmul_nf(A[k], inv);
+    const cd inv = crecip(shfl_c(g.mask, ak, src));
+    const cd l = cmul_nf(ak, inv);
 #pragma unroll
-    for (int j = k + 1; j < N; ++j) {
-      cd pj = shfl_c(g.mask, A[j], src);
-      if (!used) A[j] = csub_nf(A[j], cmul_nf(l, pj));
+    for (int j = 1; j < N; ++j) {
+      if (j > k) {  // warp-uniform test
+        const cd pj = shfl_c(g.mask, A[j], src);
+        if (!used) A[j] = csub_nf(A[j], cmul_nf(l, pj));
+      }
     }
-    cd pb = shfl_c(g.mask, b, src);
+    const cd pb = shfl_c(g.mask, b, src);
     if (!used) b = csub_nf(b, cmul_nf(l, pb));
   }
   bool fin = true;
   mine = cd{0.0, 0.0};
-#pragma unroll
+#pragma unroll 1
   for (int k = N - 1; k >= 0; --k) {
-    cd xk = cdiv(b, A[k]);
-    xk = shfl_c(g.mask, xk, g.src(pl[k]));
-    x[k] = xk;
+    const cd ak = pick<N>(A, k);
+    const unsigned who = __ballot_sync(g.mask, mystep == k) & g.bits;
+    const int src = who ? (__ffs(who) - 1) : g.lane;
+    cd xk = cdiv(b, ak);
+    xk = shfl_c(g.mask, xk, src);
     fin = fin && cfinite(xk);
     if (k == g.lg) mine = xk;
-    if (mystep < k) b = csub_nf(b, cmul_nf(A[k], xk));
+    if (mystep < k) b = csub_nf(b, cmul_nf(ak, xk));
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (j == k) A[j] = xk;
   }
   return !bad && fin;
 }
@@ -87,7 +96,7 @@ NID_D bool group_lu_solve(const Grp<N>& g, cd (&A)[N], cd b, cd (&x)[N], cd& min
 // row-major in A (leading dimension lda), run by one thread.  Columns are
 // rotated until pairwise orthogonal; the singular values are the column
 // norms.  V (n x n, ldv) accumulates the right rotations when non-null.
-NID_D void jacobi_svd(cd* A, int m, int n, int lda, cd* V, int ldv, double* sv) {
+static __device__ __noinline__ void jacobi_svd(cd* A, int m, int n, int lda, cd* V, int ldv, double* sv) {
   if (V) {
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j) V[i * ldv + j] = cd{i == j ? 1.0 : 0.0, 0.0};
@@ -169,7 +178,7 @@ NID_D void cond_rank_from_sv(const double* s_desc, int k, double tol, double& co
 // Min-norm least squares x = argmin |A x - b| with rcond 1e-14 (zgelsd
 // semantics), square or tall A (m x n, row-major lda).  A is destroyed;
 // V (n x n) and sv (n) are scratch.
-NID_D void lstsq_minnorm(cd* A, int m, int n, int lda, const cd* b, cd* V, double* sv, cd* x) {
+static __device__ __noinline__ void lstsq_minnorm(cd* A, int m, int n, int lda, const cd* b, cd* V, double* sv, cd* x) {
   jacobi_svd(A, m, n, lda, V, n, sv);
   double smax = 0.0;
   for (int j = 0; j < n; ++j) smax = fmax(smax, sv[j]);

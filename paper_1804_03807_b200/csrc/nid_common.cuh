@@ -58,6 +58,18 @@ NID_HD cd cdiv(cd a, cd b) {
   return cd{(a.re * r + a.im) / den, (a.im * r - a.re) / den};
 }
 NID_HD cd crecip(cd b) { return cdiv(cd{1.0, 0.0}, b); }
+// 1/b with a single real division: b is scaled by an exact power of two so
+// |b|^2 can neither overflow nor underflow (rounding-level equal to crecip)
+NID_D cd crecip_fast(cd b) {
+  const double m = fmax(fabs(b.re), fabs(b.im));
+  if (!(m > 0.0) || !isfinite(m)) return crecip(b);
+  const double s = ldexp(1.0, -ilogb(m));
+  const double re = b.re * s, im = b.im * s;
+  const double d = s / fma(re, re, im * im);
+  return cd{re * d, -im * d};
+}
+// |a|^2 (for max-norm comparisons: one sqrt at the end instead of a hypot per entry)
+NID_HD double cabs2(cd a) { return fma(a.re, a.re, a.im * a.im); }
 
 // max that propagates NaN like numpy's np.max
 NID_HD double nanmax(double a, double b) {
@@ -77,8 +89,10 @@ static constexpr double SINGULARITY_TOL = 1e-8;                      // linalg.p
 template <int N>
 struct Grp {
   int lane, lg, gbase, gid;  // gid: group index in warp
-  unsigned mask;
-  bool real;  // false for the leftover lanes
+  unsigned mask;  // sync mask of the *_sync intrinsics: the group's lanes (safe in
+                  // group-divergent code) or the full warp (converged compute rounds)
+  unsigned bits;  // the group's own lanes
+  bool real;      // false for the leftover lanes
   NID_D static Grp make() {
     Grp g;
     g.lane = threadIdx.x & 31;
@@ -90,7 +104,14 @@ struct Grp {
     int cnt = g.real ? N : (32 - P * N);
     unsigned m = (cnt >= 32) ? 0xffffffffu : ((1u << cnt) - 1u);
     g.mask = m << g.gbase;
+    g.bits = g.mask;
     return g;
+  }
+  // the same group, for code every lane of the warp executes together
+  NID_D Grp warpwide() const {
+    Grp w = *this;
+    w.mask = 0xffffffffu;
+    return w;
   }
   NID_D int src(int j) const { int s = gbase + j; return s < 32 ? s : lane; }
 };
@@ -130,7 +151,7 @@ template <int N>
 NID_D double group_sum(const Grp<N>& g, double v) { return group_reduce<N>(g, v, OpSum()); }
 template <int N>
 NID_D bool group_all(const Grp<N>& g, bool b) {
-  unsigned bal = __ballot_sync(g.mask, !b) & g.mask;
+  unsigned bal = __ballot_sync(g.mask, !b) & g.bits;
   return bal == 0;
 }
 

@@ -5,18 +5,22 @@
 // counter -- the GPU form of the reference's claim-guarded work crew
 // (parallel.py:37-109) -- and refill their slot the moment a path retires.
 //
-// Every loop iteration is one homotopy evaluation (H, J and, on request, the
-// noise scale) at each group's current point, followed by one group LU solve
-// if any group in the warp needs a Newton step.  What the evaluation is for
-// is decided by a per-group state machine that replays, branch for branch,
+// The warp loop alternates two uniform compute rounds -- one homotopy
+// evaluation (H, J and, on request, the noise scale) or one group LU solve
+// -- with a single copy of a control state machine.  LU rounds take
+// priority, so a group's Jacobian is never overwritten while it waits for
+// its solve.  The state machine replays, branch for branch,
 //   track           tracker.py:341-407  (secant predictor, step control,
 //                                        endgame, snap, infinity test)
 //   _correct        tracker.py:184-207  (residual-judged Newton, noise floor)
 //   _finish         tracker.py:305-338  (t=1 polish + endpoint verdict)
 //   _damped_newton  tracker.py:210-238  (8 halvings, never accept increase)
-// The endpoint Solution (condition number, regularity, double-double polish,
-// tracker.py:255-302,319-331) is computed afterwards by the endpoint kernel
-// for the paths that need one.
+// Every transition exists once in the code (the kernel must fit the
+// instruction cache); group-uniform control scalars live in shared memory,
+// only per-lane coordinates and the row/Jacobian data stay in registers.
+// The endpoint Solution (condition number, regularity, double-double
+// polish, tracker.py:255-302,319-331) is computed afterwards by the endpoint
+// kernel for the paths that need one.
 #pragma once
 #include "homotopy.cuh"
 #include "linalg.cuh"
@@ -28,6 +32,8 @@ struct TrackArgs {
   long long first_index;  // total-degree start index of path 0
   const cd* starts;       // [P][n] or null for total-degree starts
   int deg[NID_MAX_VARS];  // total-degree start degrees
+  int root_off[NID_MAX_VARS];  // offsets of each variable's roots of unity in `roots`
+  const cd* roots;             // exp(2 pi i k / d_v), k < d_v
   const cd* params;       // per-path target coefficients
   int param_div;
   unsigned long long* next;  // claim counter
@@ -40,368 +46,400 @@ struct TrackArgs {
   cd* scratch;                   // per-group lstsq scratch, 3*n*n + 2*n complex each
 };
 
-enum { M_IDLE = 0, M_CORR = 1, M_DN = 2 };
-enum { CTX_PRE = 0, CTX_STEP = 1 };
-
-template <int N>
-struct PathState {
-  long long path;
-  int mode;
-  // corrector
-  int c_ctx, c_iters, c_it, c_phase;
-  double c_tol, c_tol_eff;
-  // damped newton
-  int dn_it, dn_trial, dn_iters;
-  double dn_lam, dn_res, dn_tol;
-  // tracking
-  double t, step, prev_step, hstep, t_try, entry_norm, norm_now, move_cap, t_from;
-  int used;
-  bool have_prev, endgame;
-  // own coordinates
-  cd xo, xpo, xbo, dxo;
-  // evaluation point
-  double te;
-  bool need_scale;
-  const cd* prm;
+// control actions
+enum : int {
+  A_IDLE = 0,
+  A_EVAL,        // wait for an evaluation round at (xe, te)
+  A_SOLVE,       // wait for an LU round on the last evaluation's J
+  A_ON_EVAL,     // consume an evaluation
+  A_ON_SOLVE,    // consume a Newton step
+  A_CLAIM,       // take the next path
+  A_GATHER,      // all-gather own_next into xe, then evaluate
+  A_LOOP_TOP,    // top of track()'s while loop
+  A_CORR_DONE,   // _correct returned (c_ok, c_its)
+  A_FINISH,      // _finish: start the t=1 damped Newton
+  A_DN_CONT,     // _damped_newton loop head
+  A_DECIDE,      // _finish verdict
+  A_WRITE        // write the path's record, then claim
 };
+enum : int { M_CORR = 1, M_DN = 2 };
+enum : int { CTX_PRE = 0, CTX_STEP = 1 };
 
-template <int N>
-struct Tracker {
-  const TrackArgs& A;
-  const Grp<N>& g;
-  PathState<N>& s;
-  cd (&xe)[N];
-  unsigned long long& n_eval;
-
-  NID_D void write_result(int status, bool has_x, double t_reached, double res) {
-    long long p = s.path;
-    if (g.lg == 0) {
-      A.status[p] = (int8_t)status;
-      A.steps[p] = s.used;
-      A.t_reached[p] = t_reached;
-      A.resid[p] = res;
-    }
-    A.x_end[p * N + g.lg] = has_x ? s.xbo : cd{NAN, NAN};
-  }
-
-  NID_D void claim() {
-    unsigned long long idx = 0;
-    if (g.lg == 0) idx = atomicAdd(A.next, 1ull);
-    idx = __shfl_sync(g.mask, idx, g.gbase);
-    if ((long long)idx >= A.P) {
-      s.mode = M_IDLE;
-      s.path = -1;
-      return;
-    }
-    s.path = (long long)idx;
-    if (A.starts) {
-#pragma unroll
-      for (int v = 0; v < N; ++v) xe[v] = A.starts[s.path * N + v];
-    } else {
-      long long rem = A.first_index + s.path;
-#pragma unroll
-      for (int v = N - 1; v >= 0; --v) {
-        int d = A.deg[v];
-        long long k = rem % d;
-        rem /= d;
-        double ang = 3.141592653589793 * (2.0 * (double)k / (double)d);
-        double sn, cs;
-        sincos(ang, &sn, &cs);
-        xe[v] = cd{cs, sn};
-      }
-    }
-    s.xo = pick<N>(xe, g.lg);
-    s.prm = A.params ? A.params + (s.path / A.param_div) * A.H.nparam : nullptr;
-    s.te = 0.0;
-    start_corrector(CTX_PRE, A.prm.corrector_tol * 10.0, 3);
-  }
-
-  NID_D void start_corrector(int ctx, double tol, int iters) {
-    s.mode = M_CORR;
-    s.c_ctx = ctx;
-    s.c_tol = tol;
-    s.c_iters = iters;
-    s.c_it = 0;
-    s.c_phase = 0;
-    s.need_scale = true;
-  }
-
-  NID_D double group_max_abs_own(cd v) { return group_nanmax<N>(g, cabsd(v)); }
-
-  // top of the `while steps_used < max_steps` loop (tracker.py:367-387)
-  NID_D void loop_top() {
-    const NidTrackParams& q = A.prm;
-    if (s.used >= q.max_steps) {
-      if (s.endgame) start_finish();
-      else finish_path(NID_FAILED, false, s.t, NAN);
-      return;
-    }
-    double rem = 1.0 - s.t;
-    if (!s.endgame && s.t >= q.endgame_start) {
-      s.endgame = true;
-      s.entry_norm = group_max_abs_own(s.xo);
-    }
-    if (rem <= q.snap_remaining) {
-      start_finish();
-      return;
-    }
-    s.used += 1;
-    double hs = fmin(fmin(s.step, q.max_step), rem);
-    if (s.endgame) hs = fmin(hs, q.endgame_contraction * rem);
-    double tt = s.t + hs;
-    if (1.0 - tt < 1e-14) tt = 1.0;
-    s.hstep = hs;
-    s.t_try = tt;
-    cd xp = s.xo;
-    if (s.have_prev && s.prev_step > 0.0) xp = s.xo + (s.xo - s.xpo) * cd{hs / s.prev_step, 0.0};
-    group_gather<N>(g, xp, xe);
-    s.te = tt;
-    start_corrector(CTX_STEP, q.corrector_tol, q.max_corrector_iters);
-  }
-
-  NID_D void corrector_done(bool ok, int its) {
-    const NidTrackParams& q = A.prm;
-    if (s.c_ctx == CTX_PRE) {
-      if (!ok) {
-        s.used = 0;
-        finish_path(NID_FAILED, false, 0.0, NAN);
-        return;
-      }
-      s.xo = pick<N>(xe, g.lg);
-      s.t = 0.0;
-      s.step = q.initial_step;
-      s.have_prev = false;
-      s.prev_step = 0.0;
-      s.used = 0;
-      s.entry_norm = group_max_abs_own(s.xo);
-      s.endgame = false;
-      loop_top();
-      return;
-    }
-    if (ok) {
-      cd xn = pick<N>(xe, g.lg);
-      if (group_max_abs_own(xn) > q.infinity_threshold) {
-        finish_path(NID_AT_INFINITY, false, s.t_try, NAN);
-        return;
-      }
-      s.xpo = s.xo;
-      s.prev_step = s.hstep;
-      s.have_prev = true;
-      s.xo = xn;
-      s.t = s.t_try;
-      if (s.t >= 1.0) {
-        start_finish();
-        return;
-      }
-      if (its <= 2) s.step = fmin(s.step * 2.0, q.max_step);
-    } else {
-      s.step = s.hstep * 0.5;
-      if (s.step < q.min_step) {
-        if (s.endgame) start_finish();
-        else finish_path(NID_FAILED, false, s.t, NAN);
-        return;
-      }
-    }
-    loop_top();
-  }
-
-  // _finish, first half (tracker.py:315-317)
-  NID_D void start_finish() {
-    bool fin = group_all<N>(g, cfinite(s.xo));
-    s.norm_now = fin ? group_max_abs_own(s.xo) : INFINITY;
-    s.move_cap = 0.05 * (1.0 + s.norm_now);
-    s.t_from = s.t;
-    s.mode = M_DN;
-    s.dn_it = 0;
-    s.dn_trial = -1;
-    s.dn_iters = A.prm.final_newton_iters;
-    s.dn_tol = A.prm.corrector_tol;
-    s.xbo = s.xo;
-    group_gather<N>(g, s.xo, xe);
-    s.te = 1.0;
-    s.need_scale = false;
-  }
-
-  // _finish, verdict (tracker.py:318-338)
-  NID_D void finish_decide() {
-    const NidTrackParams& q = A.prm;
-    double res = s.dn_res;
-    bool fin = group_all<N>(g, cfinite(s.xbo));
-    double moved = fin ? group_max_abs_own(s.xbo - s.xo) : INFINITY;
-    if (isfinite(res) && res <= CONVERGED_RESIDUAL && moved <= s.move_cap) {
-      finish_path(NID_CONVERGED, true, 1.0, res);
-      return;
-    }
-    double growth = (s.norm_now + 1e-6) / (s.entry_norm + 1e-6);
-    if (s.norm_now > q.soft_infinity || growth >= 8.0) {
-      finish_path(NID_AT_INFINITY, false, s.t_from, NAN);
-      return;
-    }
-    if (isfinite(res) && res <= 1e-4 && moved <= s.move_cap) {
-      finish_path(NID_SINGULAR_ENDPOINT, true, s.t_from, res);
-      return;
-    }
-    finish_path(NID_FAILED, false, s.t_from, NAN);
-  }
-
-  NID_D void finish_path(int status, bool has_x, double t_reached, double res) {
-    write_result(status, has_x, t_reached, res);
-    claim();
-  }
-
-  // damped Newton: loop head (tracker.py:219-223)
-  NID_D bool dn_continue() {
-    if (s.dn_it >= s.dn_iters || !isfinite(s.dn_res) || s.dn_res <= s.dn_tol) {
-      finish_decide();
-      return false;
-    }
-    return true;  // solve with the Jacobian at xbo (just evaluated)
-  }
-
-  NID_D void dn_trial_point() {
-    cd xt = s.xbo + cd{s.dn_lam, 0.0} * s.dxo;
-    group_gather<N>(g, xt, xe);
-    s.te = 1.0;
-  }
-
-  // Consume an evaluation; returns true when a Newton solve is wanted.
-  NID_D bool on_eval(double resid, double scale) {
-    if (s.mode == M_CORR) {
-      if (s.c_phase == 0) s.c_tol_eff = fmax(s.c_tol, NOISE_ULPS * scale);
-      if (s.c_phase == 2 || (s.c_phase == 0 && s.c_iters == 0)) {
-        double te2 = fmax(s.c_tol, NOISE_ULPS * scale);
-        corrector_done(resid <= te2, s.c_iters);
-        return false;
-      }
-      if (!isfinite(resid)) {
-        corrector_done(false, s.c_it);
-        return false;
-      }
-      if (resid <= s.c_tol_eff) {
-        corrector_done(true, s.c_it);
-        return false;
-      }
-      return true;
-    }
-    if (s.mode == M_DN) {
-      if (s.dn_trial < 0) {
-        s.dn_res = resid;
-        return dn_continue();
-      }
-      if (isfinite(resid) && resid < s.dn_res) {  // accepted trial: new base
-        s.xbo = s.xbo + cd{s.dn_lam, 0.0} * s.dxo;
-        s.dn_res = resid;
-        s.dn_it += 1;
-        s.dn_trial = -1;
-        return dn_continue();
-      }
-      s.dn_lam *= 0.5;
-      s.dn_trial += 1;
-      if (s.dn_trial < 8) {
-        dn_trial_point();
-        return false;
-      }
-      s.dn_it += 1;  // not improved: break (tracker.py:235-237)
-      finish_decide();
-      return false;
-    }
-    return false;
-  }
-
-  // Consume the Newton step dx (full vector in every lane, mine = dx[lg]).
-  NID_D void on_solve(const cd (&dx)[N], cd mine) {
-    if (s.mode == M_CORR) {
-      bool fin = true;
-#pragma unroll
-      for (int v = 0; v < N; ++v) {
-        xe[v] = xe[v] + dx[v];
-        fin = fin && cfinite(xe[v]);
-      }
-      if (!fin) {
-        corrector_done(false, s.c_it + 1);
-        return;
-      }
-      s.c_it += 1;
-      s.c_phase = (s.c_it >= s.c_iters) ? 2 : 1;
-      s.need_scale = (s.c_phase == 2);
-      return;
-    }
-    if (s.mode == M_DN) {
-      s.dxo = mine;
-      s.dn_lam = 1.0;
-      s.dn_trial = 0;
-      dn_trial_point();
-    }
-  }
+// group-uniform control state (one copy per group, in shared memory)
+struct GroupState {
+  long long path;
+  const cd* prm;
+  double te, c_tol, c_tol_eff, dn_lam, dn_res, t, step, prev_step, hstep, t_try, entry_norm, norm_now,
+      move_cap, t_from, out_t, out_res, resid, scale;
+  int mode, c_ctx, c_iters, c_it, c_phase, c_its, dn_it, dn_trial, dn_iters, used, out_status;
+  bool c_ok, have_prev, endgame, need_scale, out_hasx, fallback;
 };
 
 template <int N>
 __global__ void __launch_bounds__(128) track_kernel(TrackArgs A) {
+  constexpr int GPW = 32 / N;  // groups per warp
+  __shared__ GroupState gs_all[4 * GPW];
   const Grp<N> g = Grp<N>::make();
-  PathState<N> s;
-  cd xe[N];
-  unsigned long long n_eval = 0, n_jac = 0, n_scale = 0, n_fb = 0;
+  const Grp<N> gw = g.warpwide();
+  const int warp = threadIdx.x >> 5;
+  GroupState& S = gs_all[warp * GPW + (g.real ? g.gid : 0)];
+  const int gslot = (blockIdx.x * blockDim.x + threadIdx.x) / 32 * GPW + g.gid;
+  const NidTrackParams& q = A.prm;
+
+  // per-lane data
+  cd xe[N];                   // the point being evaluated (full copy in every lane)
+  cd J[N];                    // Jacobian row lg of the last evaluation
+  cd hv = cd{0.0, 0.0};       // H_lg of the last evaluation
+  cd mine = cd{0.0, 0.0};     // dx[lg]
+  cd xo = cd{0.0, 0.0}, xpo = cd{0.0, 0.0}, xbo = cd{0.0, 0.0}, dxo = cd{0.0, 0.0}, own_next = cd{0.0, 0.0};
 #pragma unroll
-  for (int v = 0; v < N; ++v) xe[v] = cd{0.0, 0.0};
-  s.mode = M_IDLE;
-  s.path = -1;
-  s.need_scale = false;
-  s.te = 0.0;
-  s.prm = nullptr;
-  Tracker<N> tr{A, g, s, xe, n_eval};
-  if (g.real) tr.claim();
-  const int gslot = (blockIdx.x * blockDim.x + threadIdx.x) / 32 * (32 / N) + g.gid;
+  for (int v = 0; v < N; ++v) {
+    xe[v] = cd{0.0, 0.0};
+    J[v] = cd{0.0, 0.0};
+  }
+  unsigned long long n_eval = 0, n_jac = 0, n_scale = 0, n_fb = 0;
+  int act = g.real ? A_CLAIM : A_IDLE;
 
   while (true) {
-    const bool act = s.mode != M_IDLE;
-    if (!__any_sync(0xffffffffu, act)) break;
-    const bool ws = __any_sync(0xffffffffu, act && s.need_scale);
-    cd hv;
-    cd J[N];
-    double sS, sT;
-    eval_row<N>(A.H, act ? g.lg : N, xe, s.te, s.prm, hv, J, sS, sT, ws);
-    const double resid = group_nanmax<N>(g, cabsd(hv));
-    double scale = 0.0;
-    if (ws) {
-      double mS = group_reduce<N>(g, sS, OpMax());
-      double mT = group_reduce<N>(g, sT, OpMax());
-      scale = (1.0 - s.te) * mS + s.te * mT;
+    // ------------------------------------------------------------ control
+    while (act > A_SOLVE) {
+      switch (act) {
+        case A_CLAIM: {
+          unsigned long long idx = 0;
+          if (g.lg == 0) idx = atomicAdd(A.next, 1ull);
+          idx = __shfl_sync(g.mask, idx, g.gbase);
+          if ((long long)idx >= A.P) {
+            act = A_IDLE;
+            break;
+          }
+          const long long p = (long long)idx;
+          S.path = p;
+          if (A.starts) {
+#pragma unroll
+            for (int v = 0; v < N; ++v) xe[v] = A.starts[p * N + v];
+          } else {
+            long long rem = A.first_index + p;
+#pragma unroll
+            for (int v = N - 1; v >= 0; --v) {
+              const int d = A.deg[v];
+              const long long k = rem % d;
+              rem /= d;
+              xe[v] = A.roots[A.root_off[v] + (int)k];
+            }
+          }
+          xo = pick<N>(xe, g.lg);
+          S.prm = A.params ? A.params + (p / A.param_div) * A.H.nparam : nullptr;
+          S.te = 0.0;
+          S.used = 0;
+          S.fallback = false;
+          // _correct(h, x0, 0, tol*10, 3) precondition (tracker.py:356)
+          S.mode = M_CORR;
+          S.c_ctx = CTX_PRE;
+          S.c_tol = q.corrector_tol * 10.0;
+          S.c_iters = 3;
+          S.c_it = 0;
+          S.c_phase = 0;
+          S.need_scale = true;
+          act = A_EVAL;
+          break;
+        }
+        case A_GATHER:
+          group_gather<N>(g, own_next, xe);
+          act = A_EVAL;
+          break;
+        case A_ON_EVAL: {
+          const double resid = S.resid;
+          if (S.mode == M_CORR) {  // _correct loop body (tracker.py:191-207)
+            if (S.c_phase == 0) S.c_tol_eff = fmax(S.c_tol, NOISE_ULPS * S.scale);
+            if (S.c_phase == 2 || (S.c_phase == 0 && S.c_iters == 0)) {
+              S.c_ok = resid <= fmax(S.c_tol, NOISE_ULPS * S.scale);
+              S.c_its = S.c_iters;
+              act = A_CORR_DONE;
+            } else if (!isfinite(resid)) {
+              S.c_ok = false;
+              S.c_its = S.c_it;
+              act = A_CORR_DONE;
+            } else if (resid <= S.c_tol_eff) {
+              S.c_ok = true;
+              S.c_its = S.c_it;
+              act = A_CORR_DONE;
+            } else {
+              act = A_SOLVE;
+            }
+          } else {  // _damped_newton (tracker.py:216-238)
+            if (S.dn_trial < 0) {
+              S.dn_res = resid;
+              act = A_DN_CONT;
+            } else if (isfinite(resid) && resid < S.dn_res) {
+              xbo = xbo + cd{S.dn_lam, 0.0} * dxo;
+              S.dn_res = resid;
+              S.dn_it += 1;
+              S.dn_trial = -1;
+              act = A_DN_CONT;
+            } else {
+              S.dn_lam *= 0.5;
+              S.dn_trial += 1;
+              if (S.dn_trial < 8) {
+                own_next = xbo + cd{S.dn_lam, 0.0} * dxo;
+                act = A_GATHER;
+              } else {
+                S.dn_it += 1;  // not improved: break
+                act = A_DECIDE;
+              }
+            }
+          }
+          break;
+        }
+        case A_ON_SOLVE: {
+          if (S.mode == M_CORR) {
+            bool fin = true;
+#pragma unroll
+            for (int v = 0; v < N; ++v) {
+              xe[v] = xe[v] + J[v];  // J holds dx after an LU round
+              fin = fin && cfinite(xe[v]);
+            }
+            if (!fin) {
+              S.c_ok = false;
+              S.c_its = S.c_it + 1;
+              act = A_CORR_DONE;
+            } else {
+              S.c_it += 1;
+              S.c_phase = (S.c_it >= S.c_iters) ? 2 : 1;
+              S.need_scale = (S.c_phase == 2);
+              act = A_EVAL;
+            }
+          } else {
+            dxo = mine;
+            S.dn_lam = 1.0;
+            S.dn_trial = 0;
+            own_next = xbo + dxo;
+            act = A_GATHER;
+          }
+          break;
+        }
+        case A_CORR_DONE: {
+          if (S.c_ctx == CTX_PRE) {
+            if (!S.c_ok) {
+              S.out_status = NID_FAILED;
+              S.out_hasx = false;
+              S.out_t = 0.0;
+              S.out_res = NAN;
+              act = A_WRITE;
+              break;
+            }
+            xo = pick<N>(xe, g.lg);
+            S.t = 0.0;
+            S.step = q.initial_step;
+            S.have_prev = false;
+            S.prev_step = 0.0;
+            S.used = 0;
+            S.entry_norm = group_nanmax<N>(g, cabsd(xo));
+            S.endgame = false;
+            act = A_LOOP_TOP;
+            break;
+          }
+          if (S.c_ok) {
+            const cd xn = pick<N>(xe, g.lg);
+            if (group_nanmax<N>(g, cabsd(xn)) > q.infinity_threshold) {
+              S.out_status = NID_AT_INFINITY;
+              S.out_hasx = false;
+              S.out_t = S.t_try;
+              S.out_res = NAN;
+              act = A_WRITE;
+              break;
+            }
+            xpo = xo;
+            S.prev_step = S.hstep;
+            S.have_prev = true;
+            xo = xn;
+            S.t = S.t_try;
+            if (S.t >= 1.0) {
+              act = A_FINISH;
+              break;
+            }
+            if (S.c_its <= 2) S.step = fmin(S.step * 2.0, q.max_step);
+            act = A_LOOP_TOP;
+          } else {
+            S.step = S.hstep * 0.5;
+            if (S.step < q.min_step) {
+              if (S.endgame) {
+                act = A_FINISH;
+              } else {
+                S.out_status = NID_FAILED;
+                S.out_hasx = false;
+                S.out_t = S.t;
+                S.out_res = NAN;
+                act = A_WRITE;
+              }
+              break;
+            }
+            act = A_LOOP_TOP;
+          }
+          break;
+        }
+        case A_LOOP_TOP: {  // tracker.py:367-387
+          if (S.used >= q.max_steps) {
+            if (S.endgame) {
+              act = A_FINISH;
+            } else {
+              S.out_status = NID_FAILED;
+              S.out_hasx = false;
+              S.out_t = S.t;
+              S.out_res = NAN;
+              act = A_WRITE;
+            }
+            break;
+          }
+          const double rem = 1.0 - S.t;
+          if (!S.endgame && S.t >= q.endgame_start) {
+            S.endgame = true;
+            S.entry_norm = group_nanmax<N>(g, cabsd(xo));
+          }
+          if (rem <= q.snap_remaining) {
+            act = A_FINISH;
+            break;
+          }
+          S.used += 1;
+          double hs = fmin(fmin(S.step, q.max_step), rem);
+          if (S.endgame) hs = fmin(hs, q.endgame_contraction * rem);
+          double tt = S.t + hs;
+          if (1.0 - tt < 1e-14) tt = 1.0;
+          S.hstep = hs;
+          S.t_try = tt;
+          own_next = (S.have_prev && S.prev_step > 0.0) ? xo + (xo - xpo) * cd{hs / S.prev_step, 0.0} : xo;
+          S.te = tt;
+          S.mode = M_CORR;
+          S.c_ctx = CTX_STEP;
+          S.c_tol = q.corrector_tol;
+          S.c_iters = q.max_corrector_iters;
+          S.c_it = 0;
+          S.c_phase = 0;
+          S.need_scale = true;
+          act = A_GATHER;
+          break;
+        }
+        case A_FINISH: {  // tracker.py:315-317
+          const bool fin = group_all<N>(g, cfinite(xo));
+          S.norm_now = fin ? group_nanmax<N>(g, cabsd(xo)) : INFINITY;
+          S.move_cap = 0.05 * (1.0 + S.norm_now);
+          S.t_from = S.t;
+          S.mode = M_DN;
+          S.dn_it = 0;
+          S.dn_trial = -1;
+          S.dn_iters = q.final_newton_iters;
+          xbo = xo;
+          own_next = xo;
+          S.te = 1.0;
+          S.need_scale = false;
+          act = A_GATHER;
+          break;
+        }
+        case A_DN_CONT:  // loop head of _damped_newton
+          if (S.dn_it >= S.dn_iters || !isfinite(S.dn_res) || S.dn_res <= q.corrector_tol) act = A_DECIDE;
+          else act = A_SOLVE;
+          break;
+        case A_DECIDE: {  // tracker.py:318-338
+          const double res = S.dn_res;
+          const bool fin = group_all<N>(g, cfinite(xbo));
+          const double moved = fin ? group_nanmax<N>(g, cabsd(xbo - xo)) : INFINITY;
+          S.out_hasx = false;
+          S.out_res = NAN;
+          if (isfinite(res) && res <= CONVERGED_RESIDUAL && moved <= S.move_cap) {
+            S.out_status = NID_CONVERGED;
+            S.out_hasx = true;
+            S.out_t = 1.0;
+            S.out_res = res;
+          } else if (S.norm_now > q.soft_infinity ||
+                     (S.norm_now + 1e-6) / (S.entry_norm + 1e-6) >= 8.0) {
+            S.out_status = NID_AT_INFINITY;
+            S.out_t = S.t_from;
+          } else if (isfinite(res) && res <= 1e-4 && moved <= S.move_cap) {
+            S.out_status = NID_SINGULAR_ENDPOINT;
+            S.out_hasx = true;
+            S.out_t = S.t_from;
+            S.out_res = res;
+          } else {
+            S.out_status = NID_FAILED;
+            S.out_t = S.t_from;
+          }
+          act = A_WRITE;
+          break;
+        }
+        case A_WRITE: {
+          const long long p = S.path;
+          if (g.lg == 0) {
+            A.status[p] = (int8_t)S.out_status;
+            A.steps[p] = S.used;
+            A.t_reached[p] = S.out_t;
+            A.resid[p] = S.out_res;
+          }
+          A.x_end[p * N + g.lg] = S.out_hasx ? xbo : cd{NAN, NAN};
+          act = A_CLAIM;
+          break;
+        }
+        default:
+          act = A_IDLE;
+          break;
+      }
     }
-    bool want = false;
-    if (act) {
-      n_eval += 1;
-      n_scale += s.need_scale ? 1 : 0;
-      want = tr.on_eval(resid, scale);
-    }
-    if (__any_sync(0xffffffffu, want)) {
-      cd dx[N];
-      cd mine;
-      cd rhs = -hv;
-      bool ok = group_lu_solve<N>(g, J, rhs, dx, mine);
-      if (want) {
+
+    // ------------------------------------------------------------ compute rounds
+    // reconverge the warp: every group's lanes run the rounds together, with
+    // warp-wide masks on the collectives
+    __syncwarp();
+    if (__any_sync(0xffffffffu, act == A_SOLVE)) {
+      // LU round, in place: J becomes the Newton step dx (full copy per lane)
+      const bool ok = group_lu_solve<N>(gw, J, -hv, mine);
+      if (act == A_SOLVE) {
         n_jac += 1;
         if (!ok) {
-          // zgesv failed: min-norm least squares on the re-evaluated Jacobian
+          // zgesv failed: evaluate J again at the same point (the LU consumed
+          // it) and take the min-norm least-squares step (zgelsd) instead
           n_fb += 1;
-          cd* sc = A.scratch + (size_t)gslot * (3 * N * N + 2 * N);
-          cd hv2;
-          eval_row<N>(A.H, g.lg, xe, s.te, s.prm, hv2, J, sS, sT, false);
-#pragma unroll
-          for (int v = 0; v < N; ++v) sc[g.lg * N + v] = J[v];
-          sc[N * N + g.lg] = -hv2;
-          __syncwarp(g.mask);
-          if (g.lg == 0) {
-            double sv[N];
-            lstsq_minnorm(sc, N, N, N, sc + N * N, sc + N * N + N, sv, sc + 2 * N * N + N);
-          }
-          __syncwarp(g.mask);
-#pragma unroll
-          for (int v = 0; v < N; ++v) dx[v] = sc[2 * N * N + N + v];
-          mine = pick<N>(dx, g.lg);
-          __syncwarp(g.mask);
+          S.fallback = true;
+          act = A_EVAL;
+          continue;
         }
-        tr.on_solve(dx, mine);
+        act = A_ON_SOLVE;
       }
+      continue;
+    }
+    const bool want_eval = act == A_EVAL;
+    if (!__any_sync(0xffffffffu, want_eval)) break;
+    const bool ws = __any_sync(0xffffffffu, want_eval && S.need_scale);
+    double sS, sT;
+    const double te = want_eval ? S.te : 0.0;
+    eval_row<N>(A.H, want_eval ? g.lg : N, xe, te, want_eval ? S.prm : nullptr, hv, J, sS, sT, ws);
+    const double resid = group_nanmax<N>(gw, cabsd(hv));
+    double scale = 0.0;
+    if (ws) {
+      const double mS = group_reduce<N>(gw, sS, OpMax());
+      const double mT = group_reduce<N>(gw, sT, OpMax());
+      scale = (1.0 - te) * mS + te * mT;
+    }
+    if (want_eval && S.fallback) {
+      S.fallback = false;
+      cd* sc = A.scratch + (size_t)gslot * (3 * N * N + 2 * N);
+#pragma unroll
+      for (int v = 0; v < N; ++v) sc[g.lg * N + v] = J[v];
+      sc[N * N + g.lg] = -hv;
+      __syncwarp(g.mask);
+      if (g.lg == 0) {
+        double sv[N];
+        lstsq_minnorm(sc, N, N, N, sc + N * N, sc + N * N + N, sv, sc + 2 * N * N + N);
+      }
+      __syncwarp(g.mask);
+#pragma unroll
+      for (int v = 0; v < N; ++v) J[v] = sc[2 * N * N + N + v];
+      mine = pick<N>(J, g.lg);
+      __syncwarp(g.mask);
+      act = A_ON_SOLVE;
+    } else if (want_eval) {
+      n_eval += 1;
+      n_scale += S.need_scale ? 1 : 0;
+      S.resid = resid;
+      S.scale = scale;
+      act = A_ON_EVAL;
     }
   }
   if (g.real && g.lg == 0) {

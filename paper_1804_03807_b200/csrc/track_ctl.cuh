@@ -1,0 +1,598 @@
+// K3 + K4: the persistent path tracker -- controller warp + row-split workers.
+//
+// A block serves 32 path slots (slot l = lane l) with G warps.  Warp g
+// evaluates and eliminates the rows i == g (mod G) of all 32 slots, so every
+// warp walks ONE row's term table for 32 different paths: the evaluation
+// loops are warp-uniform (coefficients and exponents are broadcast loads,
+// absent variables are skipped by uniform branches, the point sits in
+// registers).  Each path's augmented Jacobian [J | -H] lives in shared
+// memory laid out [element][slot] -- every warp access is one conflict-free
+// 512-byte transaction whatever each path's row permutation.
+//
+// Warp 0 is also the controller: lane l runs slot l's state machine, whose
+// state lives in shared memory (struct of arrays), claims new paths from a
+// global atomic counter -- the GPU form of the reference's claim-guarded
+// work crew (parallel.py:37-109) -- and publishes the next evaluation point.
+// Per block iteration: control -> evaluation (all warps) -> control ->
+// LU (all warps) -> back substitution + control (warp 0), separated by block
+// barriers.  The state machine replays, branch for branch,
+//   track           tracker.py:341-407  (secant predictor, step control,
+//                                        endgame, snap, infinity test)
+//   _correct        tracker.py:184-207  (residual-judged Newton, noise floor)
+//   _finish         tracker.py:305-338  (t=1 polish + endpoint verdict)
+//   _damped_newton  tracker.py:210-238  (8 halvings, never accept increase)
+// newton_step (linalg.py:35-51) is an LU with LAPACK's partial pivoting
+// (izamax on |Re|+|Im| in row-swap order, unfused updates) with the zgelsd
+// min-norm fallback (solved by the controller lane on a global scratch copy).
+#pragma once
+#include "track_rows.cuh"
+
+namespace ctl {
+
+using rows::A;
+using rows::SLOTS;
+
+// slot state, struct of arrays [field][slot]
+enum DField {
+  D_TE, D_CTOL, D_CTOLEFF, D_DNLAM, D_DNRES, D_T, D_STEP, D_PREV, D_HSTEP, D_TTRY, D_ENTRY, D_NORMNOW,
+  D_MOVECAP, D_TFROM, D_OUTT, D_OUTRES, D_RESID, D_SCALE, D_COUNT
+};
+enum IField {
+  I_ACT, I_MODE, I_CTX, I_CITERS, I_CIT, I_CPHASE, I_CITS, I_DNIT, I_DNTRIAL, I_USED, I_OUTST, I_FLAGS, I_COUNT
+};
+enum Flag { F_COK = 1, F_HAVEPREV = 2, F_ENDGAME = 4, F_NEEDSCALE = 8, F_HASX = 16, F_FALLBACK = 32 };
+
+template <int N>
+struct Lay {
+  static constexpr int G = rows::groups<N>();
+  // complex [item][slot]
+  static constexpr int AUG = 0;              // N*(N+1) augmented matrix
+  static constexpr int XE = N * (N + 1);     // evaluation point
+  static constexpr int XO = XE + N;          // accepted point
+  static constexpr int XS = XO + N;          // x_prev / damped-Newton base
+  static constexpr int DS = XS + N;          // damped-Newton direction
+  static constexpr int CPLX = DS + N;
+  // doubles [item][slot]: slot state + per-group partial maxima / pivot exchange
+  static constexpr int DST = 0;
+  static constexpr int PART = D_COUNT;       // 3*G: r2, sS, sT per group (reused for pivot key/pos)
+  static constexpr int DBL = PART + 3 * G;
+  // long long [item][slot]: path index, parameter row
+  static constexpr int LLN = 2;
+  static constexpr size_t bytes() {
+    return (size_t)SLOTS * (CPLX * sizeof(cd) + DBL * sizeof(double) + LLN * sizeof(long long) +
+                            I_COUNT * sizeof(int));
+  }
+};
+
+}  // namespace ctl
+
+
+namespace ctl {
+
+// per-slot shared-memory views for the controller lane
+struct SlotView {
+  cd *xes, *xos, *xss, *dss;
+  double* dsl;
+  int* isl;
+  long long* lsl;
+};
+
+#define DS_(f) V.dsl[(f) * SLOTS]
+#define IS_(f) V.isl[(f) * SLOTS]
+#define HAS(fl) ((IS_(I_FLAGS) & (fl)) != 0)
+#define SETF(fl, on) (IS_(I_FLAGS) = (on) ? (IS_(I_FLAGS) | (fl)) : (IS_(I_FLAGS) & ~(fl)))
+
+// The controller: runs slot transitions until the slot needs an evaluation
+// or a solve, or goes idle.  dxv: the Newton step just solved (A_ON_SOLVE).
+// Not inlined: one copy of the state machine in the binary.
+template <int N>
+__device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, const cd* dxv) {
+  constexpr int S = SLOTS;
+  const NidTrackParams& q = Ar.prm;
+  cd* const xes = V.xes;
+  cd* const xos = V.xos;
+  cd* const xss = V.xss;
+  cd* const dss = V.dss;
+  long long* const lsl = V.lsl;
+  int act = IS_(I_ACT);
+  while (true) {
+    if (act == A_EVAL || act == A_SOLVE || act == A_IDLE) break;
+
+      if (act == A_CLAIM) {
+        const unsigned long long idx = atomicAdd(Ar.next, 1ull);
+        if ((long long)idx >= Ar.P) {
+          act = A_IDLE;
+          break;
+        }
+        const long long path = (long long)idx;
+        lsl[0] = path;
+        lsl[S] = Ar.params ? (path / Ar.param_div) * Ar.H.nparam : -1;
+        if (Ar.starts) {
+          for (int v = 0; v < N; ++v) xes[v * S] = Ar.starts[path * N + v];
+        } else {
+          long long rem = Ar.first_index + path;
+          for (int v = N - 1; v >= 0; --v) {
+            const int d = Ar.deg[v];
+            const long long k = rem % d;
+            rem /= d;
+            xes[v * S] = Ar.roots[Ar.root_off[v] + (int)k];
+          }
+        }
+        DS_(D_TE) = 0.0;
+        IS_(I_USED) = 0;
+        IS_(I_FLAGS) = F_NEEDSCALE;
+        IS_(I_MODE) = M_CORR;  // precondition _correct(h, x0, 0, tol*10, 3) (tracker.py:356)
+        IS_(I_CTX) = CTX_PRE;
+        DS_(D_CTOL) = q.corrector_tol * 10.0;
+        IS_(I_CITERS) = 3;
+        IS_(I_CIT) = 0;
+        IS_(I_CPHASE) = 0;
+        act = A_EVAL;
+        break;
+      }
+      if (act == A_ON_EVAL) {
+        const double resid = DS_(D_RESID), scale = DS_(D_SCALE);
+        if (IS_(I_MODE) == M_CORR) {  // _correct loop body (tracker.py:191-207)
+          const int ph = IS_(I_CPHASE);
+          if (ph == 0) DS_(D_CTOLEFF) = fmax(DS_(D_CTOL), NOISE_ULPS * scale);
+          if (ph == 2 || (ph == 0 && IS_(I_CITERS) == 0)) {
+            SETF(F_COK, resid <= fmax(DS_(D_CTOL), NOISE_ULPS * scale));
+            IS_(I_CITS) = IS_(I_CITERS);
+            act = A_CORR_DONE;
+          } else if (!isfinite(resid)) {
+            SETF(F_COK, false);
+            IS_(I_CITS) = IS_(I_CIT);
+            act = A_CORR_DONE;
+          } else if (resid <= DS_(D_CTOLEFF)) {
+            SETF(F_COK, true);
+            IS_(I_CITS) = IS_(I_CIT);
+            act = A_CORR_DONE;
+          } else {
+            act = A_SOLVE;
+            break;
+          }
+        } else {  // _damped_newton (tracker.py:216-238)
+          if (IS_(I_DNTRIAL) < 0) {
+            DS_(D_DNRES) = resid;
+            act = A_DN_CONT;
+          } else if (isfinite(resid) && resid < DS_(D_DNRES)) {
+            for (int v = 0; v < N; ++v) xss[v * S] = xes[v * S];  // accepted trial = new base
+            DS_(D_DNRES) = resid;
+            IS_(I_DNIT) += 1;
+            IS_(I_DNTRIAL) = -1;
+            act = A_DN_CONT;
+          } else {
+            const double lam = DS_(D_DNLAM) * 0.5;
+            DS_(D_DNLAM) = lam;
+            IS_(I_DNTRIAL) += 1;
+            if (IS_(I_DNTRIAL) < 8) {
+              for (int v = 0; v < N; ++v) xes[v * S] = xss[v * S] + cd{lam, 0.0} * dss[v * S];
+              act = A_EVAL;
+              break;
+            }
+            IS_(I_DNIT) += 1;  // not improved: break
+            act = A_DECIDE;
+          }
+        }
+        continue;
+      }
+      if (act == A_ON_SOLVE) {  // tracker.py:200-205 / 223-233
+        if (IS_(I_MODE) == M_CORR) {
+          bool fin = true;
+          for (int v = 0; v < N; ++v) {
+            const cd x = xes[v * S] + dxv[v];
+            xes[v * S] = x;
+            fin = fin && cfinite(x);
+          }
+          if (!fin) {
+            SETF(F_COK, false);
+            IS_(I_CITS) = IS_(I_CIT) + 1;
+            act = A_CORR_DONE;
+            continue;
+          }
+          IS_(I_CIT) += 1;
+          IS_(I_CPHASE) = (IS_(I_CIT) >= IS_(I_CITERS)) ? 2 : 1;
+          SETF(F_NEEDSCALE, IS_(I_CPHASE) == 2);
+          act = A_EVAL;
+          break;
+        }
+        DS_(D_DNLAM) = 1.0;
+        IS_(I_DNTRIAL) = 0;
+        for (int v = 0; v < N; ++v) {
+          dss[v * S] = dxv[v];
+          xes[v * S] = xss[v * S] + dxv[v];
+        }
+        act = A_EVAL;
+        break;
+      }
+      if (act == A_CORR_DONE) {
+        if (IS_(I_CTX) == CTX_PRE) {
+          if (!HAS(F_COK)) {
+            IS_(I_OUTST) = NID_FAILED;
+            SETF(F_HASX, false);
+            DS_(D_OUTT) = 0.0;
+            act = A_WRITE;
+            continue;
+          }
+          double m = 0.0;
+          for (int v = 0; v < N; ++v) {
+            const cd x = xes[v * S];
+            xos[v * S] = x;
+            m = nanmax(m, cabsd(x));
+          }
+          DS_(D_T) = 0.0;
+          DS_(D_STEP) = q.initial_step;
+          SETF(F_HAVEPREV, false);
+          SETF(F_ENDGAME, false);
+          DS_(D_PREV) = 0.0;
+          IS_(I_USED) = 0;
+          DS_(D_ENTRY) = m;
+          act = A_LOOP_TOP;
+          continue;
+        }
+        if (HAS(F_COK)) {
+          double m = 0.0;
+          for (int v = 0; v < N; ++v) m = nanmax(m, cabsd(xes[v * S]));
+          if (m > q.infinity_threshold) {
+            IS_(I_OUTST) = NID_AT_INFINITY;
+            SETF(F_HASX, false);
+            DS_(D_OUTT) = DS_(D_TTRY);
+            act = A_WRITE;
+            continue;
+          }
+          for (int v = 0; v < N; ++v) {
+            xss[v * S] = xos[v * S];  // x_prev <- x
+            xos[v * S] = xes[v * S];  // x <- x_new
+          }
+          DS_(D_PREV) = DS_(D_HSTEP);
+          SETF(F_HAVEPREV, true);
+          DS_(D_T) = DS_(D_TTRY);
+          if (DS_(D_T) >= 1.0) {
+            act = A_FINISH;
+            continue;
+          }
+          if (IS_(I_CITS) <= 2) DS_(D_STEP) = fmin(DS_(D_STEP) * 2.0, q.max_step);
+          act = A_LOOP_TOP;
+        } else {
+          const double st = DS_(D_HSTEP) * 0.5;
+          DS_(D_STEP) = st;
+          if (st < q.min_step) {
+            if (HAS(F_ENDGAME)) {
+              act = A_FINISH;
+            } else {
+              IS_(I_OUTST) = NID_FAILED;
+              SETF(F_HASX, false);
+              DS_(D_OUTT) = DS_(D_T);
+              act = A_WRITE;
+            }
+            continue;
+          }
+          act = A_LOOP_TOP;
+        }
+        continue;
+      }
+      if (act == A_LOOP_TOP) {  // tracker.py:367-387
+        if (IS_(I_USED) >= q.max_steps) {
+          if (HAS(F_ENDGAME)) {
+            act = A_FINISH;
+          } else {
+            IS_(I_OUTST) = NID_FAILED;
+            SETF(F_HASX, false);
+            DS_(D_OUTT) = DS_(D_T);
+            act = A_WRITE;
+          }
+          continue;
+        }
+        const double t = DS_(D_T);
+        const double rem = 1.0 - t;
+        if (!HAS(F_ENDGAME) && t >= q.endgame_start) {
+          SETF(F_ENDGAME, true);
+          double m = 0.0;
+          for (int v = 0; v < N; ++v) m = nanmax(m, cabsd(xos[v * S]));
+          DS_(D_ENTRY) = m;
+        }
+        if (rem <= q.snap_remaining) {
+          act = A_FINISH;
+          continue;
+        }
+        IS_(I_USED) += 1;
+        double hs = fmin(fmin(DS_(D_STEP), q.max_step), rem);
+        if (HAS(F_ENDGAME)) hs = fmin(hs, q.endgame_contraction * rem);
+        double tt = t + hs;
+        if (1.0 - tt < 1e-14) tt = 1.0;
+        DS_(D_HSTEP) = hs;
+        DS_(D_TTRY) = tt;
+        const double prev = DS_(D_PREV);
+        if (HAS(F_HAVEPREV) && prev > 0.0) {
+          const cd ratio = cd{hs / prev, 0.0};
+          for (int v = 0; v < N; ++v) {
+            const cd xo = xos[v * S];
+            xes[v * S] = xo + (xo - xss[v * S]) * ratio;
+          }
+        } else {
+          for (int v = 0; v < N; ++v) xes[v * S] = xos[v * S];
+        }
+        DS_(D_TE) = tt;
+        IS_(I_MODE) = M_CORR;
+        IS_(I_CTX) = CTX_STEP;
+        DS_(D_CTOL) = q.corrector_tol;
+        IS_(I_CITERS) = q.max_corrector_iters;
+        IS_(I_CIT) = 0;
+        IS_(I_CPHASE) = 0;
+        SETF(F_NEEDSCALE, true);
+        act = A_EVAL;
+        break;
+      }
+      if (act == A_FINISH) {  // tracker.py:315-317
+        bool fin = true;
+        double m = 0.0;
+        for (int v = 0; v < N; ++v) {
+          const cd x = xos[v * S];
+          fin = fin && cfinite(x);
+          m = nanmax(m, cabsd(x));
+          xss[v * S] = x;  // damped-Newton base x1 <- x
+          xes[v * S] = x;
+        }
+        const double nn = fin ? m : INFINITY;
+        DS_(D_NORMNOW) = nn;
+        DS_(D_MOVECAP) = 0.05 * (1.0 + nn);
+        DS_(D_TFROM) = DS_(D_T);
+        IS_(I_MODE) = M_DN;
+        IS_(I_DNIT) = 0;
+        IS_(I_DNTRIAL) = -1;
+        DS_(D_TE) = 1.0;
+        SETF(F_NEEDSCALE, false);
+        act = A_EVAL;
+        break;
+      }
+      if (act == A_DN_CONT) {  // loop head of _damped_newton
+        const double r = DS_(D_DNRES);
+        if (IS_(I_DNIT) >= q.final_newton_iters || !isfinite(r) || r <= q.corrector_tol) {
+          act = A_DECIDE;
+          continue;
+        }
+        act = A_SOLVE;
+        break;
+      }
+      if (act == A_DECIDE) {  // tracker.py:318-338
+        const double res = DS_(D_DNRES);
+        bool finb = true;
+        double moved = 0.0;
+        for (int v = 0; v < N; ++v) {
+          const cd xb = xss[v * S];
+          finb = finb && cfinite(xb);
+          moved = nanmax(moved, cabsd(xb - xos[v * S]));
+        }
+        if (!finb) moved = INFINITY;
+        const double cap = DS_(D_MOVECAP), nn = DS_(D_NORMNOW);
+        SETF(F_HASX, false);
+        DS_(D_OUTRES) = NAN;
+        if (isfinite(res) && res <= CONVERGED_RESIDUAL && moved <= cap) {
+          IS_(I_OUTST) = NID_CONVERGED;
+          SETF(F_HASX, true);
+          DS_(D_OUTT) = 1.0;
+          DS_(D_OUTRES) = res;
+        } else if (nn > q.soft_infinity || (nn + 1e-6) / (DS_(D_ENTRY) + 1e-6) >= 8.0) {
+          IS_(I_OUTST) = NID_AT_INFINITY;
+          DS_(D_OUTT) = DS_(D_TFROM);
+        } else if (isfinite(res) && res <= 1e-4 && moved <= cap) {
+          IS_(I_OUTST) = NID_SINGULAR_ENDPOINT;
+          SETF(F_HASX, true);
+          DS_(D_OUTT) = DS_(D_TFROM);
+          DS_(D_OUTRES) = res;
+        } else {
+          IS_(I_OUTST) = NID_FAILED;
+          DS_(D_OUTT) = DS_(D_TFROM);
+        }
+        act = A_WRITE;
+        continue;
+      }
+      if (act == A_WRITE) {
+        const long long path = lsl[0];
+        const bool hx = HAS(F_HASX);
+        Ar.status[path] = (int8_t)IS_(I_OUTST);
+        Ar.steps[path] = IS_(I_USED);
+        Ar.t_reached[path] = DS_(D_OUTT);
+        Ar.resid[path] = hx ? DS_(D_OUTRES) : NAN;
+        for (int v = 0; v < N; ++v) Ar.x_end[path * N + v] = hx ? xss[v * S] : cd{NAN, NAN};
+        act = A_CLAIM;
+        continue;
+      }
+      act = A_IDLE;  // A_IDLE / unknown
+      break;
+    }
+    IS_(I_ACT) = act;
+}
+
+#undef DS_
+#undef IS_
+#undef HAS
+#undef SETF
+
+}  // namespace ctl
+
+template <int N>
+__global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(const __grid_constant__ TrackArgs Ar) {
+  using namespace ctl;
+  using L = Lay<N>;
+  constexpr int G = L::G;
+  constexpr int S = SLOTS;
+  extern __shared__ __align__(16) unsigned char smem_ctl[];
+  const int lane = threadIdx.x & 31;
+  const int g = threadIdx.x >> 5;
+  cd* const cb = reinterpret_cast<cd*>(smem_ctl);
+  double* const db = reinterpret_cast<double*>(cb + (size_t)L::CPLX * S);
+  long long* const lb = reinterpret_cast<long long*>(db + (size_t)L::DBL * S);
+  int* const ib = reinterpret_cast<int*>(lb + (size_t)L::LLN * S);
+  cd* const aug = cb + lane;
+  cd* const xes = cb + L::XE * S + lane;
+  cd* const xos = cb + L::XO * S + lane;
+  cd* const xss = cb + L::XS * S + lane;
+  cd* const dss = cb + L::DS * S + lane;
+  double* const dsl = db + lane;  // slot doubles: dsl[f * S]
+  double* const part = db + L::PART * S + lane;
+  int* const isl = ib + lane;
+  long long* const lsl = lb + lane;
+  const NidTrackParams& q = Ar.prm;
+  unsigned long long n_eval = 0, n_jac = 0, n_scale = 0, n_fb = 0;
+
+#define DS_(f) dsl[(f) * S]
+#define IS_(f) isl[(f) * S]
+#define HAS(fl) ((IS_(I_FLAGS) & (fl)) != 0)
+#define SETF(fl, on) (IS_(I_FLAGS) = (on) ? (IS_(I_FLAGS) | (fl)) : (IS_(I_FLAGS) & ~(fl)))
+
+  if (g == 0) IS_(I_ACT) = A_CLAIM;
+  const SlotView V{xes, xos, xss, dss, dsl, isl, lsl};
+
+  while (true) {
+    if (g == 0) control<N>(Ar, V, nullptr);
+    // ------------------------------------------------------------ evaluation
+    if (!__syncthreads_or(IS_(I_ACT) != A_IDLE)) break;
+    const bool want_eval = IS_(I_ACT) == A_EVAL;
+    const bool ws = want_eval && HAS(F_NEEDSCALE | F_FALLBACK);
+    if (want_eval) {
+      cd x[N];
+#pragma unroll
+      for (int v = 0; v < N; ++v) x[v] = xes[v * S];
+      const long long pr = lsl[S];
+      const cd* prm = pr >= 0 ? Ar.params + pr : nullptr;
+      rows::eval_rows<N>(Ar.H, g, x, DS_(D_TE), prm, aug, part, ws);
+    }
+    __syncthreads();
+    if (g == 0 && want_eval) {
+      double sc = 0.0;
+      const double r = rows::combine_resid<N>(aug, part, DS_(D_TE), sc);
+      if (HAS(F_FALLBACK)) {
+        // zgesv failed at this point: min-norm least squares (zgelsd) on the
+        // re-evaluated augmented matrix
+        SETF(F_FALLBACK, false);
+        cd* sc2 = Ar.scratch + (size_t)(blockIdx.x * S + lane) * (3 * N * N + 2 * N);
+        for (int i = 0; i < N; ++i) {
+          for (int j = 0; j < N; ++j) sc2[i * N + j] = A<N>(aug, i, j);
+          sc2[N * N + i] = A<N>(aug, i, N);
+        }
+        double sv[N];
+        lstsq_minnorm(sc2, N, N, N, sc2 + N * N, sc2 + N * N + N, sv, sc2 + 2 * N * N + N);
+        IS_(I_ACT) = A_ON_SOLVE;
+        control<N>(Ar, V, sc2 + 2 * N * N + N);
+      } else {
+        n_eval += 1;
+        n_scale += HAS(F_NEEDSCALE) ? 1 : 0;
+        DS_(D_RESID) = r;
+        DS_(D_SCALE) = sc;
+        IS_(I_ACT) = A_ON_EVAL;
+        control<N>(Ar, V, nullptr);
+      }
+    }
+    // ------------------------------------------------------------ LU
+    if (__syncthreads_or(IS_(I_ACT) == A_SOLVE)) {
+      const bool solving = IS_(I_ACT) == A_SOLVE;
+      double* const pk_key = part;               // per group (reuses the partial maxima)
+      double* const pk_pos = part + G * S;
+      unsigned long long perm = 0, pinv = 0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        perm |= (unsigned long long)i << (4 * i);
+        pinv |= (unsigned long long)i << (4 * i);
+      }
+      bool bad = false;
+#pragma unroll 1
+      for (int k = 0; k < N; ++k) {
+        if (solving) {  // local pivot candidates among my physical rows
+          double best = -1.0;
+          int bpos = N;
+#pragma unroll
+          for (int r = g; r < N; r += G) {
+            const int pos = (pinv >> (4 * r)) & 15;
+            if (pos >= k) {
+              const double key = cabs1(A<N>(aug, r, k));
+              if (key > best || (key == best && pos < bpos)) {
+                best = key;
+                bpos = pos;
+              }
+            }
+          }
+          pk_key[g * S] = best;
+          pk_pos[g * S] = (double)bpos;
+        }
+        __syncthreads();
+        int r0 = 0;
+        if (solving) {
+          double best = -1.0;
+          int pk = k;
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+            const double key = pk_key[gg * S];
+            const int pos = (int)pk_pos[gg * S];
+            if (pos < N && (key > best || (key == best && pos < pk))) {
+              best = key;
+              pk = pos;
+            }
+          }
+          if (!(best > 0.0)) bad = true;
+          const unsigned long long rk = (perm >> (4 * k)) & 15, rp = (perm >> (4 * pk)) & 15;
+          perm &= ~((15ull << (4 * k)) | (15ull << (4 * pk)));
+          perm |= (rp << (4 * k)) | (rk << (4 * pk));
+          pinv &= ~((15ull << (4 * rk)) | (15ull << (4 * rp)));
+          pinv |= ((unsigned long long)k << (4 * rp)) | ((unsigned long long)pk << (4 * rk));
+          r0 = (int)rp;
+          cd prow[N + 1];
+#pragma unroll
+          for (int j = 1; j <= N; ++j)
+            if (j > k) prow[j] = A<N>(aug, r0, j);
+          const cd inv = crecip_fast(A<N>(aug, r0, k));
+#pragma unroll 1
+          for (int r = g; r < N; r += G) {
+            const int pos = (pinv >> (4 * r)) & 15;
+            if (pos > k) {
+              const cd l = cmul_nf(A<N>(aug, r, k), inv);
+#pragma unroll
+              for (int j = 1; j <= N; ++j) {
+                if (j > k) {
+                  cd& a = A<N>(aug, r, j);
+                  a = csub_nf(a, cmul_nf(l, prow[j]));
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+        if (solving && g == r0 % G) A<N>(aug, r0, k) = crecip_fast(A<N>(aug, r0, k));
+      }
+      __syncthreads();
+      if (g == 0 && solving) {
+        n_jac += 1;
+        cd dx[N];
+        bool fin = true;
+#pragma unroll
+        for (int k = N - 1; k >= 0; --k) {
+          const int r = (perm >> (4 * k)) & 15;
+          cd s = A<N>(aug, r, N);
+#pragma unroll
+          for (int j = k + 1; j < N; ++j) s = csub_nf(s, cmul_nf(A<N>(aug, r, j), dx[j]));
+          dx[k] = cmul_nf(s, A<N>(aug, r, k));
+          fin = fin && cfinite(dx[k]);
+        }
+        if (!bad && fin) {
+          IS_(I_ACT) = A_ON_SOLVE;
+          control<N>(Ar, V, dx);
+        } else {
+          n_fb += 1;
+          SETF(F_FALLBACK, true);
+          IS_(I_ACT) = A_EVAL;  // re-evaluate the same point, then lstsq
+        }
+      }
+      __syncthreads();
+    }
+  }
+#undef DS_
+#undef IS_
+#undef HAS
+#undef SETF
+  if (g == 0) {
+    atomicAdd(Ar.counters + 0, n_eval);
+    atomicAdd(Ar.counters + 1, n_jac);
+    atomicAdd(Ar.counters + 2, n_scale);
+    atomicAdd(Ar.counters + 3, n_fb);
+  }
+}

@@ -52,8 +52,17 @@ class FlopModel:
 
 
 def flop_model(low: Lowered) -> FlopModel:
+    """Counts over the merged start+target term table (a closed-form
+    total-degree start is counted as its two terms per row, as in §8(d))."""
     n = low.n
-    ex = [tuple(int(v) for v in row[:n]) for row in low.expo]
+    ex = []
+    for i in range(n):
+        row = {tuple(int(v) for v in e[:n]) for e in low.expo[low.row_off[i]:low.row_off[i + 1]]}
+        if low.start_degrees is not None:
+            e = [0] * n
+            e[i] = int(low.start_degrees[i])
+            row |= {tuple(e), (0,) * n}
+        ex.extend(sorted(row))
     mono = {e for e in ex if sum(e) >= 2}
     dmono = set()
     nnz = 0

@@ -66,6 +66,7 @@ class Lowered:
     pslot: np.ndarray | None  # int8 [T]
     nparam: int
     gamma: complex
+    start_degrees: np.ndarray | None = None  # int32 [n] when the start is total degree
 
     @property
     def nterms(self) -> int:
@@ -85,12 +86,14 @@ def lower(start, target, gamma: complex = 1.0 + 0j, param_terms: dict | None = N
     if n > _lib.MAX_VARS:
         raise ValueError(f"at most {_lib.MAX_VARS} variables are supported")
     param_terms = param_terms or {}
+    tdeg = total_degree_degrees(start)
     offs = [0]
     ex, cs, ct, sl = [], [], [], []
     for i in range(n):
         acc: dict[tuple, list] = {}
-        for e, c in start.polys[i].terms:
-            acc.setdefault(tuple(int(v) for v in e), [0j, 0j])[0] += complex(c)
+        if tdeg is None:  # a total-degree start is evaluated in closed form instead
+            for e, c in start.polys[i].terms:
+                acc.setdefault(tuple(int(v) for v in e), [0j, 0j])[0] += complex(c)
         for e, c in target.polys[i].terms:
             acc.setdefault(tuple(int(v) for v in e), [0j, 0j])[1] += complex(c)
         for (r, e), _ in param_terms.items():
@@ -113,7 +116,25 @@ def lower(start, target, gamma: complex = 1.0 + 0j, param_terms: dict | None = N
     pslot = np.array(sl, dtype=np.int8) if param_terms else None
     nparam = (max(param_terms.values()) + 1) if param_terms else 0
     return Lowered(n, np.array(offs, dtype=np.int32), expo, np.array(cs, dtype=np.complex128),
-                   np.array(ct, dtype=np.complex128), pslot, nparam, complex(gamma))
+                   np.array(ct, dtype=np.complex128), pslot, nparam, complex(gamma),
+                   None if tdeg is None else np.array(tdeg, dtype=np.int32))
+
+
+def total_degree_degrees(start) -> list[int] | None:
+    """d_i when row i of `start` is exactly x_i^{d_i} - 1 for every i, else None."""
+    n = start.nvars
+    if len(start.polys) != n:
+        return None
+    degs = []
+    for i, p in enumerate(start.polys):
+        terms = dict((tuple(int(v) for v in e), complex(c)) for e, c in p.terms)
+        if len(terms) != 2 or terms.get((0,) * n) != -1.0 + 0j:
+            return None
+        (e, c), = [(e, c) for e, c in terms.items() if any(e)]
+        if c != 1.0 + 0j or sum(1 for v in e if v) != 1 or e[i] < 1:
+            return None
+        degs.append(int(e[i]))
+    return degs
 
 
 class DeviceHomotopy:
@@ -122,10 +143,11 @@ class DeviceHomotopy:
     def __init__(self, low: Lowered):
         L = _lib.lib()
         self.low = low
-        self._keep = (low.row_off, low.expo, low.cs, low.ct, low.pslot)
+        self._keep = (low.row_off, low.expo, low.cs, low.ct, low.pslot, low.start_degrees)
         d = _lib.HomotopyDescC(
             low.n, low.nterms, _lib.ptr(low.row_off), _lib.ptr(low.expo), _lib.ptr(low.cs), _lib.ptr(low.ct),
-            _lib.ptr(low.pslot), low.nparam, low.gamma.real, low.gamma.imag)
+            _lib.ptr(low.pslot), low.nparam, low.gamma.real, low.gamma.imag,
+            0 if low.start_degrees is None else 1, _lib.ptr(low.start_degrees))
         h = C.c_void_p()
         _lib.check(L.nid_homotopy_create(C.byref(d), C.byref(h)), L)
         self.handle = h

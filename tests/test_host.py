@@ -33,16 +33,25 @@ def test_linear_homotopy_shape_check():
 def test_lowering_merges_rows():
     p = configs.c5()
     low = lower(p.start, p.target, p.gamma)
-    assert low.n == 10 and low.nterms == 110
-    # every start and target term is present with its coefficient
+    # the total-degree start is recognised and evaluated in closed form
+    assert list(low.start_degrees) == list(range(1, 11))
+    assert low.n == 10 and low.nterms == 92 and not np.any(low.cs)
     for i in range(10):
         seg = slice(low.row_off[i], low.row_off[i + 1])
         ex = [tuple(e[:10]) for e in low.expo[seg]]
         assert ex == sorted(ex)
-        got_t = {e: c for e, c in zip(ex, low.ct[seg]) if c != 0}
-        assert got_t == dict(p.target.polys[i].terms)
-        got_s = {e: c for e, c in zip(ex, low.cs[seg]) if c != 0}
-        assert got_s == dict(p.start.polys[i].terms)
+        assert {e: c for e, c in zip(ex, low.ct[seg]) if c != 0} == dict(p.target.polys[i].terms)
+    # a generic start is merged term by term
+    pd = configs.c3_mini()
+    E = pd.emb.system
+    g = PolySystem(E.nvars, tuple(make_poly(E.nvars, [(e, 2 * c) for e, c in q.terms]) for q in E.polys))
+    low = lower(g, E, 0.5j)
+    assert low.start_degrees is None
+    for i in range(E.nvars):
+        seg = slice(low.row_off[i], low.row_off[i + 1])
+        ex = [tuple(e[:E.nvars]) for e in low.expo[seg]]
+        assert {e: c for e, c in zip(ex, low.cs[seg]) if c != 0} == dict(g.polys[i].terms)
+        assert {e: c for e, c in zip(ex, low.ct[seg]) if c != 0} == dict(E.polys[i].terms)
 
 
 def test_lowering_param_slots_for_membership():
@@ -123,7 +132,7 @@ def test_no_gpu_means_loud_failure():
 
 def test_ctypes_struct_layout_matches_header():
     assert ctypes.sizeof(_lib.TrackParamsC) == 4 * 8 + 2 * 4 + 4 * 8 + 2 * 4 + 8 + 2 * 4
-    assert ctypes.sizeof(_lib.HomotopyDescC) == 4 + 4 + 5 * 8 + 8 + 16  # n, nterms, 5 ptrs, nparam(+pad), gamma
+    assert ctypes.sizeof(_lib.HomotopyDescC) == 4 + 4 + 5 * 8 + 8 + 16 + 8 + 8  # ..., start_kind(+pad), degrees
 
 
 @pytest.mark.parametrize("total,world", [(3628800, 8), (5040, 3), (7, 4), (0, 2)])
