@@ -2,6 +2,7 @@
 // Host-side plumbing only: uploads lowered homotopies, stages host buffers,
 // sizes the persistent grids and dispatches to the per-size kernels.
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -9,7 +10,7 @@
 #include "aux_kernels.cuh"
 #include "endpoint.cuh"
 #include "launch.h"
-#include "track.cuh"
+#include "track_common.cuh"
 #include "track_ctl.cuh"
 
 static thread_local std::string g_err;
@@ -33,6 +34,8 @@ static int g_device = -1;
 struct NidHomotopy {
   int n, nterms, nparam, maxdeg, multilinear, td;
   int tddeg[NID_MAX_VARS];
+  int grow[NID_MAX_VARS];
+  int goff[17];
   cd gamma;
   int* row_off;
   uint4* expo;
@@ -48,6 +51,8 @@ struct NidHomotopy {
     h.multilinear = multilinear;
     h.td = td;
     for (int v = 0; v < NID_MAX_VARS; ++v) h.tddeg[v] = tddeg[v];
+    for (int v = 0; v < NID_MAX_VARS; ++v) h.grow[v] = grow[v];
+    for (int v = 0; v <= 16; ++v) h.goff[v] = goff[v];
     h.row_off = row_off;
     h.expo = expo;
     h.cs = cs;
@@ -185,6 +190,41 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   h->multilinear = maxdeg <= 1 ? 1 : 0;
   h->td = d->start_kind == 1 ? 1 : 0;
   for (int v = 0; v < NID_MAX_VARS; ++v) h->tddeg[v] = (h->td && v < n) ? d->start_degrees[v] : 0;
+  // tracker row groups (rows::groups<n>()): longest-processing-time assignment
+  // of rows to warp groups by evaluation cost (terms x their variable count)
+  {
+    const int G = n <= 3 ? 1 : (n <= 6 ? 2 : (n <= 10 ? 4 : 8));
+    std::vector<std::pair<double, int>> cost;
+    for (int i = 0; i < n; ++i) {
+      double c = h->td ? 2.0 + h->tddeg[i] : 0.0;
+      for (int k = off[i]; k < off[i + 1]; ++k) {
+        int nz = 0;
+        for (int v = 0; v < n; ++v) nz += d->expo[k * NID_MAX_VARS + v] ? 1 : 0;
+        c += 4.0 + 3.0 * nz;
+      }
+      cost.push_back({c, i});
+    }
+    std::sort(cost.begin(), cost.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
+      return a.first > b.first || (a.first == b.first && a.second < b.second);
+    });
+    std::vector<std::vector<int>> grp(G);
+    std::vector<double> load(G, 0.0);
+    for (auto& cr : cost) {
+      int best = 0;
+      for (int gg = 1; gg < G; ++gg)
+        if (load[gg] < load[best]) best = gg;
+      grp[best].push_back(cr.second);
+      load[best] += cr.first;
+    }
+    int pos = 0;
+    for (int gg = 0; gg <= 16; ++gg) h->goff[gg] = 0;
+    for (int gg = 0; gg < G; ++gg) {
+      h->goff[gg] = pos;
+      std::sort(grp[gg].begin(), grp[gg].end());
+      for (int r : grp[gg]) h->grow[pos++] = r;
+    }
+    for (int gg = G; gg <= 16; ++gg) h->goff[gg] = pos;
+  }
   h->gamma = cd{d->gamma_re, d->gamma_im};
   const size_t Tp = T > 0 ? T : 1;
   cudaError_t e = cudaSuccess;

@@ -26,6 +26,10 @@ struct HomDev {
   int multilinear;        // every table exponent is 0 or 1
   int td;                 // start system is total degree (closed form)
   int tddeg[NID_MAX_VARS];
+  // rows of each warp group of the tracker, cost balanced on the host:
+  // group g evaluates rows grow[goff[g] .. goff[g+1])
+  int grow[NID_MAX_VARS];
+  int goff[17];
   const int* row_off;     // [n+1]
   const uint4* expo;      // [nterms], 16 exponent bytes
   const cd* cs;           // start coefficients

@@ -3,7 +3,7 @@
 // size gets fully unrolled register-resident code.
 #include "endpoint.cuh"
 #include "launch.h"
-#include "track.cuh"
+#include "track_common.cuh"
 #include "track_ctl.cuh"
 
 #ifndef NID_N

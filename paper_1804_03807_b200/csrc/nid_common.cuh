@@ -62,11 +62,22 @@ NID_HD cd crecip(cd b) { return cdiv(cd{1.0, 0.0}, b); }
 // |b|^2 can neither overflow nor underflow (rounding-level equal to crecip)
 NID_D cd crecip_fast(cd b) {
   const double m = fmax(fabs(b.re), fabs(b.im));
+  if (m > 1e-150 && m < 1e150) {  // |b|^2 safely representable: one division
+    const double d = 1.0 / fma(b.re, b.re, b.im * b.im);
+    return cd{b.re * d, -b.im * d};
+  }
   if (!(m > 0.0) || !isfinite(m)) return crecip(b);
   const double s = ldexp(1.0, -ilogb(m));
   const double re = b.re * s, im = b.im * s;
   const double d = s / fma(re, re, im * im);
   return cd{re * d, -im * d};
+}
+// |a| by one square root when |a|^2 is safely representable (hypot otherwise);
+// within an ulp of hypot
+NID_HD double cabs_fast(cd a) {
+  const double m = fmax(fabs(a.re), fabs(a.im));
+  if (m > 1e-150 && m < 1e150) return sqrt(fma(a.re, a.re, a.im * a.im));
+  return hypot(a.re, a.im);
 }
 // |a|^2 (for max-norm comparisons: one sqrt at the end instead of a hypot per entry)
 NID_HD double cabs2(cd a) { return fma(a.re, a.re, a.im * a.im); }

@@ -9,13 +9,15 @@
 // memory laid out [element][slot] -- every warp access is one conflict-free
 // 512-byte transaction whatever each path's row permutation.
 //
-// Warp 0 is also the controller: lane l runs slot l's state machine, whose
-// state lives in shared memory (struct of arrays), claims new paths from a
-// global atomic counter -- the GPU form of the reference's claim-guarded
-// work crew (parallel.py:37-109) -- and publishes the next evaluation point.
-// Per block iteration: control -> evaluation (all warps) -> control ->
-// LU (all warps) -> back substitution + control (warp 0), separated by block
-// barriers.  The state machine replays, branch for branch,
+// Lanes 0..32/G-1 of every warp are controllers: each runs one slot's state
+// machine, whose state lives in shared memory (struct of arrays), claims new
+// paths from a global atomic counter -- the GPU form of the reference's
+// claim-guarded work crew (parallel.py:37-109) -- publishes the next
+// evaluation point and back-substitutes its slot's Newton step.  Per block
+// iteration: control -> [barrier] evaluation (all warps, row groups) ->
+// [barrier] control -> LU of the warp's own slots (warp-local) -> back
+// substitution + control.  Only the two block barriers couple the warps.
+// The state machine replays, branch for branch,
 //   track           tracker.py:341-407  (secant predictor, step control,
 //                                        endgame, snap, infinity test)
 //   _correct        tracker.py:184-207  (residual-judged Newton, noise floor)
@@ -38,7 +40,8 @@ enum DField {
   D_MOVECAP, D_TFROM, D_OUTT, D_OUTRES, D_RESID, D_SCALE, D_COUNT
 };
 enum IField {
-  I_ACT, I_MODE, I_CTX, I_CITERS, I_CIT, I_CPHASE, I_CITS, I_DNIT, I_DNTRIAL, I_USED, I_OUTST, I_FLAGS, I_COUNT
+  I_ACT, I_MODE, I_CTX, I_CITERS, I_CIT, I_CPHASE, I_CITS, I_DNIT, I_DNTRIAL, I_USED, I_OUTST, I_FLAGS, I_BAD,
+  I_COUNT
 };
 enum Flag { F_COK = 1, F_HAVEPREV = 2, F_ENDGAME = 4, F_NEEDSCALE = 8, F_HASX = 16, F_FALLBACK = 32 };
 
@@ -56,8 +59,8 @@ struct Lay {
   static constexpr int DST = 0;
   static constexpr int PART = D_COUNT;       // 3*G: r2, sS, sT per group (reused for pivot key/pos)
   static constexpr int DBL = PART + 3 * G;
-  // long long [item][slot]: path index, parameter row
-  static constexpr int LLN = 2;
+  // long long [item][slot]: path index, parameter row, LU row permutation
+  static constexpr int LLN = 3;
   static constexpr size_t bytes() {
     return (size_t)SLOTS * (CPLX * sizeof(cd) + DBL * sizeof(double) + LLN * sizeof(long long) +
                             I_COUNT * sizeof(int));
@@ -218,7 +221,7 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
           for (int v = 0; v < N; ++v) {
             const cd x = xes[v * S];
             xos[v * S] = x;
-            m = nanmax(m, cabsd(x));
+            m = nanmax(m, cabs_fast(x));
           }
           DS_(D_T) = 0.0;
           DS_(D_STEP) = q.initial_step;
@@ -232,7 +235,7 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
         }
         if (HAS(F_COK)) {
           double m = 0.0;
-          for (int v = 0; v < N; ++v) m = nanmax(m, cabsd(xes[v * S]));
+          for (int v = 0; v < N; ++v) m = nanmax(m, cabs_fast(xes[v * S]));
           if (m > q.infinity_threshold) {
             IS_(I_OUTST) = NID_AT_INFINITY;
             SETF(F_HASX, false);
@@ -288,7 +291,7 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
         if (!HAS(F_ENDGAME) && t >= q.endgame_start) {
           SETF(F_ENDGAME, true);
           double m = 0.0;
-          for (int v = 0; v < N; ++v) m = nanmax(m, cabsd(xos[v * S]));
+          for (int v = 0; v < N; ++v) m = nanmax(m, cabs_fast(xos[v * S]));
           DS_(D_ENTRY) = m;
         }
         if (rem <= q.snap_remaining) {
@@ -329,7 +332,7 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
         for (int v = 0; v < N; ++v) {
           const cd x = xos[v * S];
           fin = fin && cfinite(x);
-          m = nanmax(m, cabsd(x));
+          m = nanmax(m, cabs_fast(x));
           xss[v * S] = x;  // damped-Newton base x1 <- x
           xes[v * S] = x;
         }
@@ -361,7 +364,7 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
         for (int v = 0; v < N; ++v) {
           const cd xb = xss[v * S];
           finb = finb && cfinite(xb);
-          moved = nanmax(moved, cabsd(xb - xos[v * S]));
+          moved = nanmax(moved, cabs_fast(xb - xos[v * S]));
         }
         if (!finb) moved = INFINITY;
         const double cap = DS_(D_MOVECAP), nn = DS_(D_NORMNOW);
@@ -417,6 +420,7 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
   using L = Lay<N>;
   constexpr int G = L::G;
   constexpr int S = SLOTS;
+  constexpr int CPW = S / G;  // controller slots per warp
   extern __shared__ __align__(16) unsigned char smem_ctl[];
   const int lane = threadIdx.x & 31;
   const int g = threadIdx.x >> 5;
@@ -424,172 +428,181 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
   double* const db = reinterpret_cast<double*>(cb + (size_t)L::CPLX * S);
   long long* const lb = reinterpret_cast<long long*>(db + (size_t)L::DBL * S);
   int* const ib = reinterpret_cast<int*>(lb + (size_t)L::LLN * S);
+  // worker view: this thread evaluates/eliminates rows of slot `lane`
   cd* const aug = cb + lane;
-  cd* const xes = cb + L::XE * S + lane;
-  cd* const xos = cb + L::XO * S + lane;
-  cd* const xss = cb + L::XS * S + lane;
-  cd* const dss = cb + L::DS * S + lane;
-  double* const dsl = db + lane;  // slot doubles: dsl[f * S]
   double* const part = db + L::PART * S + lane;
-  int* const isl = ib + lane;
-  long long* const lsl = lb + lane;
-  const NidTrackParams& q = Ar.prm;
+  // controller view: lanes < CPW of warp g run the state machine of slot cs
+  const bool is_ctl = lane < CPW;
+  const int cs = g * CPW + (lane % CPW);
+  cd* const augc = cb + cs;
+  double* const partc = db + L::PART * S + cs;
+  const SlotView V{cb + L::XE * S + cs, cb + L::XO * S + cs, cb + L::XS * S + cs, cb + L::DS * S + cs, db + cs,
+                   ib + cs, lb + cs};
   unsigned long long n_eval = 0, n_jac = 0, n_scale = 0, n_fb = 0;
 
-#define DS_(f) dsl[(f) * S]
-#define IS_(f) isl[(f) * S]
-#define HAS(fl) ((IS_(I_FLAGS) & (fl)) != 0)
-#define SETF(fl, on) (IS_(I_FLAGS) = (on) ? (IS_(I_FLAGS) | (fl)) : (IS_(I_FLAGS) & ~(fl)))
+#define W_IS(f) ib[(f) * S + lane]   // worker's slot
+#define W_DS(f) db[(f) * S + lane]
+#define C_IS(f) V.isl[(f) * S]       // controller's slot
+#define C_DS(f) V.dsl[(f) * S]
 
-  if (g == 0) IS_(I_ACT) = A_CLAIM;
-  const SlotView V{xes, xos, xss, dss, dsl, isl, lsl};
+  if (is_ctl) C_IS(I_ACT) = A_CLAIM;
 
   while (true) {
-    if (g == 0) control<N>(Ar, V, nullptr);
+    if (is_ctl) control<N>(Ar, V, nullptr);
     // ------------------------------------------------------------ evaluation
-    if (!__syncthreads_or(IS_(I_ACT) != A_IDLE)) break;
-    const bool want_eval = IS_(I_ACT) == A_EVAL;
-    const bool ws = want_eval && HAS(F_NEEDSCALE | F_FALLBACK);
-    if (want_eval) {
+    if (!__syncthreads_or(W_IS(I_ACT) != A_IDLE)) break;
+    if (W_IS(I_ACT) == A_EVAL) {
       cd x[N];
 #pragma unroll
-      for (int v = 0; v < N; ++v) x[v] = xes[v * S];
-      const long long pr = lsl[S];
+      for (int v = 0; v < N; ++v) x[v] = cb[(L::XE + v) * S + lane];
+      const long long pr = lb[S + lane];
       const cd* prm = pr >= 0 ? Ar.params + pr : nullptr;
-      rows::eval_rows<N>(Ar.H, g, x, DS_(D_TE), prm, aug, part, ws);
+      rows::eval_rows<N>(Ar.H, g, x, W_DS(D_TE), prm, aug, part, (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0);
     }
     __syncthreads();
-    if (g == 0 && want_eval) {
+    if (is_ctl && C_IS(I_ACT) == A_EVAL) {
       double sc = 0.0;
-      const double r = rows::combine_resid<N>(aug, part, DS_(D_TE), sc);
-      if (HAS(F_FALLBACK)) {
+      const double r = rows::combine_resid<N>(augc, partc, C_DS(D_TE), sc);
+      if (C_IS(I_FLAGS) & F_FALLBACK) {
         // zgesv failed at this point: min-norm least squares (zgelsd) on the
         // re-evaluated augmented matrix
-        SETF(F_FALLBACK, false);
-        cd* sc2 = Ar.scratch + (size_t)(blockIdx.x * S + lane) * (3 * N * N + 2 * N);
+        C_IS(I_FLAGS) &= ~F_FALLBACK;
+        cd* sc2 = Ar.scratch + (size_t)(blockIdx.x * S + cs) * (3 * N * N + 2 * N);
         for (int i = 0; i < N; ++i) {
-          for (int j = 0; j < N; ++j) sc2[i * N + j] = A<N>(aug, i, j);
-          sc2[N * N + i] = A<N>(aug, i, N);
+          for (int j = 0; j < N; ++j) sc2[i * N + j] = A<N>(augc, i, j);
+          sc2[N * N + i] = A<N>(augc, i, N);
         }
         double sv[N];
         lstsq_minnorm(sc2, N, N, N, sc2 + N * N, sc2 + N * N + N, sv, sc2 + 2 * N * N + N);
-        IS_(I_ACT) = A_ON_SOLVE;
+        C_IS(I_ACT) = A_ON_SOLVE;
         control<N>(Ar, V, sc2 + 2 * N * N + N);
       } else {
         n_eval += 1;
-        n_scale += HAS(F_NEEDSCALE) ? 1 : 0;
-        DS_(D_RESID) = r;
-        DS_(D_SCALE) = sc;
-        IS_(I_ACT) = A_ON_EVAL;
+        n_scale += (C_IS(I_FLAGS) & F_NEEDSCALE) ? 1 : 0;
+        C_DS(D_RESID) = r;
+        C_DS(D_SCALE) = sc;
+        C_IS(I_ACT) = A_ON_EVAL;
         control<N>(Ar, V, nullptr);
       }
     }
-    // ------------------------------------------------------------ LU
-    if (__syncthreads_or(IS_(I_ACT) == A_SOLVE)) {
-      const bool solving = IS_(I_ACT) == A_SOLVE;
-      double* const pk_key = part;               // per group (reuses the partial maxima)
-      double* const pk_pos = part + G * S;
-      unsigned long long perm = 0, pinv = 0;
+    // ------------------------------------------------------------ LU (warp-local)
+    // Warp g factorizes the CPW slots it controls: lane = q * CPW + sl (slot
+    // sl, row group q; physical rows r == q (mod G)).  Slot-minor lanes keep
+    // every quarter-warp on 8 different slots, i.e. different banks of the
+    // [element][slot] layout.  Pivots are reduced over the slot's G lanes
+    // (stride CPW) by shuffles; __syncwarp orders the shared-memory updates.
+    __syncwarp();
+    {
+      const int sl = lane % CPW, q = lane / CPW;
+      const int ss = g * CPW + sl;  // slot factorized by this lane
+      cd* const augs = cb + ss;
+      const bool solving = ib[I_ACT * S + ss] == A_SOLVE;
+      if (__any_sync(0xffffffffu, solving)) {
+        unsigned long long perm = 0, pinv = 0;
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        perm |= (unsigned long long)i << (4 * i);
-        pinv |= (unsigned long long)i << (4 * i);
-      }
-      bool bad = false;
+        for (int i = 0; i < N; ++i) {
+          perm |= (unsigned long long)i << (4 * i);
+          pinv |= (unsigned long long)i << (4 * i);
+        }
+        bool bad = false;
 #pragma unroll 1
-      for (int k = 0; k < N; ++k) {
-        if (solving) {  // local pivot candidates among my physical rows
+        for (int k = 0; k < N; ++k) {
           double best = -1.0;
           int bpos = N;
+          if (solving) {
 #pragma unroll
-          for (int r = g; r < N; r += G) {
-            const int pos = (pinv >> (4 * r)) & 15;
-            if (pos >= k) {
-              const double key = cabs1(A<N>(aug, r, k));
-              if (key > best || (key == best && pos < bpos)) {
-                best = key;
-                bpos = pos;
-              }
-            }
-          }
-          pk_key[g * S] = best;
-          pk_pos[g * S] = (double)bpos;
-        }
-        __syncthreads();
-        int r0 = 0;
-        if (solving) {
-          double best = -1.0;
-          int pk = k;
-#pragma unroll
-          for (int gg = 0; gg < G; ++gg) {
-            const double key = pk_key[gg * S];
-            const int pos = (int)pk_pos[gg * S];
-            if (pos < N && (key > best || (key == best && pos < pk))) {
-              best = key;
-              pk = pos;
-            }
-          }
-          if (!(best > 0.0)) bad = true;
-          const unsigned long long rk = (perm >> (4 * k)) & 15, rp = (perm >> (4 * pk)) & 15;
-          perm &= ~((15ull << (4 * k)) | (15ull << (4 * pk)));
-          perm |= (rp << (4 * k)) | (rk << (4 * pk));
-          pinv &= ~((15ull << (4 * rk)) | (15ull << (4 * rp)));
-          pinv |= ((unsigned long long)k << (4 * rp)) | ((unsigned long long)pk << (4 * rk));
-          r0 = (int)rp;
-          cd prow[N + 1];
-#pragma unroll
-          for (int j = 1; j <= N; ++j)
-            if (j > k) prow[j] = A<N>(aug, r0, j);
-          const cd inv = crecip_fast(A<N>(aug, r0, k));
-#pragma unroll 1
-          for (int r = g; r < N; r += G) {
-            const int pos = (pinv >> (4 * r)) & 15;
-            if (pos > k) {
-              const cd l = cmul_nf(A<N>(aug, r, k), inv);
-#pragma unroll
-              for (int j = 1; j <= N; ++j) {
-                if (j > k) {
-                  cd& a = A<N>(aug, r, j);
-                  a = csub_nf(a, cmul_nf(l, prow[j]));
+            for (int r = q; r < N; r += G) {
+              const int pos = (pinv >> (4 * r)) & 15;
+              if (pos >= k) {
+                const double key = cabs1(A<N>(augs, r, k));
+                if (key > best || (key == best && pos < bpos)) {
+                  best = key;
+                  bpos = pos;
                 }
               }
             }
           }
-        }
-        __syncthreads();
-        if (solving && g == r0 % G) A<N>(aug, r0, k) = crecip_fast(A<N>(aug, r0, k));
-      }
-      __syncthreads();
-      if (g == 0 && solving) {
-        n_jac += 1;
-        cd dx[N];
-        bool fin = true;
 #pragma unroll
-        for (int k = N - 1; k >= 0; --k) {
-          const int r = (perm >> (4 * k)) & 15;
-          cd s = A<N>(aug, r, N);
+          for (int m = CPW; m < 32; m <<= 1) {  // first max of |Re|+|Im| in logical order
+            const double ok = __shfl_xor_sync(0xffffffffu, best, m);
+            const int op = __shfl_xor_sync(0xffffffffu, bpos, m);
+            if (op < N && (bpos >= N || ok > best || (ok == best && op < bpos))) {
+              best = ok;
+              bpos = op;
+            }
+          }
+          if (solving) {
+            const int pk = bpos < N ? bpos : k;
+            if (!(best > 0.0)) bad = true;
+            const unsigned long long rk = (perm >> (4 * k)) & 15, rp = (perm >> (4 * pk)) & 15;
+            perm &= ~((15ull << (4 * k)) | (15ull << (4 * pk)));
+            perm |= (rp << (4 * k)) | (rk << (4 * pk));
+            pinv &= ~((15ull << (4 * rk)) | (15ull << (4 * rp)));
+            pinv |= ((unsigned long long)k << (4 * rp)) | ((unsigned long long)pk << (4 * rk));
+            const int r0 = (int)rp;
+            cd prow[N + 1];
 #pragma unroll
-          for (int j = k + 1; j < N; ++j) s = csub_nf(s, cmul_nf(A<N>(aug, r, j), dx[j]));
-          dx[k] = cmul_nf(s, A<N>(aug, r, k));
-          fin = fin && cfinite(dx[k]);
+            for (int j = 1; j <= N; ++j)
+              if (j > k) prow[j] = A<N>(augs, r0, j);
+            const cd inv = crecip_fast(A<N>(augs, r0, k));
+#pragma unroll 1
+            for (int r = q; r < N; r += G) {
+              const int pos = (pinv >> (4 * r)) & 15;
+              if (pos > k) {
+                const cd l = cmul_nf(A<N>(augs, r, k), inv);
+#pragma unroll
+                for (int j = 1; j <= N; ++j) {
+                  if (j > k) {
+                    cd& a = A<N>(augs, r, j);
+                    a = csub_nf(a, cmul_nf(l, prow[j]));
+                  }
+                }
+              }
+            }
+            __syncwarp();
+            // the pivot's reciprocal replaces it (the back substitution multiplies)
+            if (q == r0 % G) A<N>(augs, r0, k) = inv;
+          } else {
+            __syncwarp();
+          }
+          __syncwarp();
         }
-        if (!bad && fin) {
-          IS_(I_ACT) = A_ON_SOLVE;
-          control<N>(Ar, V, dx);
-        } else {
-          n_fb += 1;
-          SETF(F_FALLBACK, true);
-          IS_(I_ACT) = A_EVAL;  // re-evaluate the same point, then lstsq
+        if (solving && q == 0) {
+          lb[2 * S + ss] = (long long)perm;
+          ib[I_BAD * S + ss] = bad ? 1 : 0;
         }
       }
-      __syncthreads();
+    }
+    __syncwarp();
+    if (is_ctl && C_IS(I_ACT) == A_SOLVE) {  // back substitution by the slot's controller
+      n_jac += 1;
+      const unsigned long long pm = (unsigned long long)V.lsl[2 * S];
+      cd dx[N];
+      bool fin = true;
+#pragma unroll
+      for (int k = N - 1; k >= 0; --k) {
+        const int r = (pm >> (4 * k)) & 15;
+        cd s = A<N>(augc, r, N);
+#pragma unroll
+        for (int j = k + 1; j < N; ++j) s = csub_nf(s, cmul_nf(A<N>(augc, r, j), dx[j]));
+        dx[k] = cmul_nf(s, A<N>(augc, r, k));
+        fin = fin && cfinite(dx[k]);
+      }
+      if (!C_IS(I_BAD) && fin) {
+        C_IS(I_ACT) = A_ON_SOLVE;
+        control<N>(Ar, V, dx);
+      } else {
+        n_fb += 1;
+        C_IS(I_FLAGS) |= F_FALLBACK;
+        C_IS(I_ACT) = A_EVAL;  // re-evaluate the same point, then lstsq
+      }
     }
   }
-#undef DS_
-#undef IS_
-#undef HAS
-#undef SETF
-  if (g == 0) {
+#undef W_IS
+#undef W_DS
+#undef C_IS
+#undef C_DS
+  if (is_ctl) {
     atomicAdd(Ar.counters + 0, n_eval);
     atomicAdd(Ar.counters + 1, n_jac);
     atomicAdd(Ar.counters + 2, n_scale);
