@@ -164,3 +164,54 @@ def random_slices(n: int, count: int, seed: int) -> np.ndarray:
     decision 2)."""
     gen = rngmod.stream(seed, rngmod.CONFIG_CANDIDATES, 2)
     return rngmod.random_complex(gen, count * (n - 2) * (n + 1)).reshape(count, n - 2, n + 1)
+
+
+def slice_homotopy(pd: PositiveDimensional, gamma_seed: int = 0):
+    """Total-degree homotopy onto {h1 = h2 = 0} cut by n-2 hyperplanes whose
+    coefficients are per-path parameters (one slice per 2^2 = 4 paths): the
+    C4 on-component sampler as a single launch."""
+    from .homotopy import LinearHomotopy, lower
+
+    n = pd.f.nvars
+    template = component_slice_system(pd, np.ones((n - 2, n + 1)))
+    start = total_degree_start(template)
+    slots = {}
+    for j in range(n - 2):
+        for l in range(n + 1):
+            e = [0] * n
+            if l:
+                e[l - 1] = 1
+            slots[(2 + j, tuple(e))] = j * (n + 1) + l
+    gamma = rngmod.gamma_for(gamma_seed if gamma_seed else pd.seed, 7)
+    low = lower(start, template, gamma, slots)
+    return low, tuple(template.degrees())
+
+
+def c4_candidates(pd: PositiveDimensional, n_on: int, n_off: int, seed: int, params=None):
+    """n_on points on the component (random 2-dim slices, 4 points each,
+    tracked on the GPU) and n_off iid complex N(0,1) points; returns
+    (candidates [n_on + n_off, n], labels)."""
+    from .homotopy import DeviceHomotopy, TrackParams
+    from .tracker import track_batch
+
+    n = pd.f.nvars
+    n_slices = (n_on + 3) // 4
+    low, degrees = slice_homotopy(pd)
+    dev = DeviceHomotopy(low)
+    hyper = random_slices(n, n_slices, seed)  # (slices, n-2, n+1)
+    prm = hyper.reshape(n_slices, -1)
+    paths = 4 * n_slices
+    starts = np.tile(total_degree_starts_np(degrees), (n_slices, 1))
+    res = track_batch(dev, starts, params or TrackParams(), target_params=prm, param_div=4)
+    ok = res.succeeded
+    on = res.x[ok][:n_on]
+    off = membership_candidates_offcomponent(n, n_off, seed)
+    cands = np.concatenate([on, off])
+    labels = np.concatenate([np.ones(len(on), np.int8), np.zeros(len(off), np.int8)])
+    return cands, labels, {"slices": n_slices, "slice_paths": paths, "slice_finite": int(ok.sum())}
+
+
+def total_degree_starts_np(degrees):
+    from .systems import total_degree_starts
+
+    return total_degree_starts(degrees)

@@ -1,0 +1,58 @@
+"""C3 (n=8 embedded to 14 variables) and C4 membership on the GPU.
+
+C3: the top-level continuation finds exactly the 4 zero-slack witness points
+of the degree-4 component {h1 = h2 = 0} (known answer), and the cascade
+levels satisfy starts = at_infinity + zero + nonzero + failures.
+C4: membership verdicts equal the labels known by construction
+(on-component points from random slices, off-component random points).
+"""
+
+import numpy as np
+import pytest
+
+from paper_1804_03807_b200 import cascade, configs, filtering
+from paper_1804_03807_b200.homotopy import TrackParams
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c3_top(nid):
+    pd = configs.c3()
+    top, stats = cascade.solve_top(pd.emb, return_arrays=True)
+    lv = cascade._classify_level(top, pd.emb, pd.emb.k, TrackParams())
+    return pd, top, stats, lv
+
+
+def test_c3_top_witness_degree_is_four(c3_top):
+    pd, top, stats, lv = c3_top
+    assert stats.continuation_paths == 4 ** 8
+    assert len(lv.zero_slack) == 4  # degree of {h1 = h2 = 0}
+    n = pd.emb.n_original
+    for s in lv.zero_slack:
+        x = s.coordinates[:n]
+        from oracle import nid_oracle as O
+        from paper_1804_03807_b200.polys import PolySystem
+        hv = O.eval_system(PolySystem(n, (pd.h1, pd.h2)), x)
+        assert np.max(np.abs(hv)) < 1e-8
+
+
+def test_c3_cascade_accounting(c3_top):
+    pd, top, stats, lv = c3_top
+    sup = cascade.run_cascade(top, pd.emb)
+    assert [l.dimension for l in sup.levels] == list(range(6, -1, -1))
+    for l in sup.levels:
+        c = l.counts
+        assert c["starts"] == c["at_infinity"] + c["zero_slack"] + c["nonzero_slack"] + c["failures"]
+    for a, b in zip(sup.levels, sup.levels[1:]):
+        assert b.starts == len(a.nonzero_slack)
+
+
+def test_c4_membership_matches_construction(c3_top):
+    pd, top, stats, lv = c3_top
+    W = filtering.WitnessSet(pd.emb.k, pd.emb, lv.zero_slack)
+    cands, labels, info = configs.c4_candidates(pd, 200, 200, 44)
+    assert info["slice_finite"] == info["slice_paths"]
+    verdict, tracked = filtering.membership_batch(W, cands)
+    assert tracked == 4 * len(cands) - 4 * int(np.sum(verdict[:0]))
+    assert np.all((verdict == 1) == (labels == 1))
