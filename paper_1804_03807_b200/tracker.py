@@ -107,7 +107,18 @@ def _device_of(h) -> DeviceHomotopy:
         return h
     if isinstance(h, LinearHomotopy):
         return h.device()
+    if all(hasattr(h, a) for a in ("start", "target", "gamma")):
+        # a reference nidpipe.tracker.LinearHomotopy (duck-typed: only
+        # .start/.target/.gamma and .polys[i].terms are read)
+        cache = _FOREIGN.get(id(h))
+        if cache is None or cache[0] is not h:
+            cache = (h, LinearHomotopy(h.start, h.target, complex(h.gamma)))
+            _FOREIGN[id(h)] = cache
+        return cache[1].device()
     raise TypeError("expected a LinearHomotopy (the GPU path tracks lowered linear homotopies)")
+
+
+_FOREIGN: dict = {}
 
 
 def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=None, first_index: int = 0,
