@@ -23,8 +23,13 @@ OBJ = os.path.join(ROOT, "build", "nid")
 LIB = os.path.join(PKG, "libnid.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         "-I" + os.path.join(ROOT, "include")]
 SIZES = list(range(1, 17))
+if os.environ.get("NID_PHASE_TIMERS"):
+    FLAGS = FLAGS + ["-DNID_PHASE_TIMERS"]
+if os.environ.get("NID_G10"):
+    FLAGS = FLAGS + ["-DNID_G10=" + os.environ["NID_G10"]]
 
 
 def _sources():
@@ -66,7 +71,7 @@ def build(jobs: int | None = None, verbose: bool = False, force: bool = False) -
                 if verbose and out.strip():
                     print(out)
     if cmds or force or not os.path.exists(LIB) or any(os.path.getmtime(x) > os.path.getmtime(LIB) for x in objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lnvrtc"])
     return LIB
 
 

@@ -1,6 +1,8 @@
 // libnid.so: the C-ABI boundary (declared in include/nid.h).
 // Host-side plumbing only: uploads lowered homotopies, stages host buffers,
 // sizes the persistent grids and dispatches to the per-size kernels.
+#include <nvrtc.h>
+
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
@@ -15,6 +17,7 @@
 
 static thread_local std::string g_err;
 static NidCounters g_counters = {};
+static unsigned long long g_phase[7] = {};
 static int g_device = -1;
 
 #define FAIL(msg)          \
@@ -42,6 +45,8 @@ struct NidHomotopy {
   cd *cs, *ct;
   double *acs, *act;
   int8_t* pslot;
+  cudaLibrary_t jit_lib = nullptr;  // NVRTC-specialised tracker (nid_homotopy_jit)
+  cudaKernel_t jit_kernel = nullptr;
   HomDev dev() const {
     HomDev h;
     h.n = n;
@@ -105,6 +110,7 @@ static const EvalFn k_eval[17] = NID_TABLE(launch_eval_);
 static const NewtonFn k_newton[17] = NID_TABLE(launch_newton_);
 static const RegsFn k_regs[17] = NID_TABLE(track_regs_);
 static const RegsFn k_tthreads[17] = NID_TABLE(track_threads_);
+static const RegsFn k_tsmem[17] = NID_TABLE(track_smem_);
 
 static int sm_count() {
   int dev = 0, sms = 148;
@@ -193,7 +199,7 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   // tracker row groups (rows::groups<n>()): longest-processing-time assignment
   // of rows to warp groups by evaluation cost (terms x their variable count)
   {
-    const int G = n <= 3 ? 1 : (n <= 6 ? 2 : (n <= 10 ? 4 : 8));
+    const int G = rows::groups_for(n);
     std::vector<std::pair<double, int>> cost;
     for (int i = 0; i < n; ++i) {
       double c = h->td ? 2.0 + h->tddeg[i] : 0.0;
@@ -252,8 +258,57 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   return 0;
 }
 
+int nid_homotopy_jit(NidHomotopy* h, const char* src, const char* include_dirs, char* log, int logcap) {
+  if (!h || !src) FAIL("null argument");
+  if (log && logcap > 0) log[0] = 0;
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src, "nid_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) FAIL("nvrtcCreateProgram failed");
+  char name[64];
+  snprintf(name, sizeof(name), "track_ctl_kernel<%d, JitEval>", h->n);
+  nvrtcAddNameExpression(prog, name);
+  std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-default-device"};
+  if (include_dirs) {
+    std::string dirs(include_dirs);
+    size_t pos = 0;
+    while (pos <= dirs.size()) {
+      size_t e = dirs.find(':', pos);
+      if (e == std::string::npos) e = dirs.size();
+      if (e > pos) opts.push_back("-I" + dirs.substr(pos, e - pos));
+      pos = e + 1;
+    }
+  }
+  std::vector<const char*> copts;
+  for (auto& o : opts) copts.push_back(o.c_str());
+  nvrtcResult rc = nvrtcCompileProgram(prog, (int)copts.size(), copts.data());
+  size_t lsz = 0;
+  nvrtcGetProgramLogSize(prog, &lsz);
+  std::string lg(lsz, '\0');
+  if (lsz) nvrtcGetProgramLog(prog, &lg[0]);
+  if (log && logcap > 0) snprintf(log, (size_t)logcap, "%s", lg.c_str());
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    g_err = "NVRTC compile failed: " + lg.substr(0, 2000);
+    return 3;
+  }
+  const char* lowered = nullptr;
+  nvrtcGetLoweredName(prog, name, &lowered);
+  std::string lname = lowered ? lowered : "";
+  size_t csz = 0;
+  nvrtcGetCUBINSize(prog, &csz);
+  std::vector<char> cubin(csz);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  if (h->jit_lib) cudaLibraryUnload(h->jit_lib);
+  h->jit_lib = nullptr;
+  h->jit_kernel = nullptr;
+  CK(cudaLibraryLoadData(&h->jit_lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+  CK(cudaLibraryGetKernel(&h->jit_kernel, h->jit_lib, lname.c_str()));
+  return 0;
+}
+
 int nid_homotopy_destroy(NidHomotopy* h) {
   if (!h) return 0;
+  if (h->jit_lib) cudaLibraryUnload(h->jit_lib);
   cudaFree(h->row_off);
   cudaFree(h->expo);
   cudaFree(h->cs);
@@ -262,6 +317,14 @@ int nid_homotopy_destroy(NidHomotopy* h) {
   cudaFree(h->act);
   if (h->pslot) cudaFree(h->pslot);
   delete h;
+  return 0;
+}
+
+int nid_track_groups(int n) { return (n < 1 || n > 16) ? -1 : rows::groups_for(n); }
+
+int nid_phase_cycles(unsigned long long* out7) {
+  if (!out7) FAIL("null argument");
+  for (int i = 0; i < 7; ++i) out7[i] = g_phase[i];
   return 0;
 }
 
@@ -329,9 +392,9 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
     d_reg = ws<int8_t>(W_REG, P);
     if (!d_x || !d_st || !d_steps || !d_tr || !d_res || !d_cond || !d_reg) FAIL("out of device memory (outputs)");
   }
-  unsigned long long* d_cnt = ws<unsigned long long>(W_COUNT, 8);
+  unsigned long long* d_cnt = ws<unsigned long long>(W_COUNT, 16);
   if (!d_cnt) FAIL("out of device memory (counters)");
-  CK(cudaMemsetAsync(d_cnt, 0, 8 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(d_cnt, 0, 16 * sizeof(unsigned long long), s));
 
   TrackArgs a;
   memset(&a, 0, sizeof(a));
@@ -378,7 +441,22 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
   CK(cudaEventCreate(&e1));
   CK(cudaEventCreate(&e2));
   CK(cudaEventRecord(e0, s));
-  k_track[n](a, max_blocks, s);
+  if (h->jit_kernel) {
+    const void* fn = (const void*)h->jit_kernel;
+    const int threads = 32 * rows::groups_for(n);
+    const int smem = k_tsmem[n]();
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int per = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
+    if (per < 1) per = 1;
+    long long blocks = (long long)sm_count() * per;
+    const long long need = (P + 31) / 32;
+    if (need < blocks) blocks = need;
+    void* args[] = {(void*)&a};
+    CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, (size_t)smem, s));
+  } else {
+    k_track[n](a, max_blocks, s);
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(e1, s));
 
@@ -412,8 +490,9 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
     CK(cudaMemcpyAsync(out->condition, d_cond, P * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(out->regular, d_reg, P, cudaMemcpyDeviceToHost, s));
   }
-  unsigned long long hc[8];
+  unsigned long long hc[16];
   CK(cudaMemcpyAsync(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  for (int i = 0; i < 7; ++i) g_phase[i] = hc[8 + i];
   CK(cudaStreamSynchronize(s));
   float ms1 = 0.f, ms2 = 0.f;
   cudaEventElapsedTime(&ms1, e0, e1);

@@ -72,4 +72,6 @@ int CAT(track_regs_, NID_N)() {
 
 int CAT(track_threads_, NID_N)() { return rows::SLOTS; }  // path slots per block
 
+int CAT(track_smem_, NID_N)() { return (int)ctl::Lay<NID_N>::bytes(); }
+
 }  // namespace nid

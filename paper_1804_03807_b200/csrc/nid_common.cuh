@@ -1,11 +1,24 @@
 // Common device arithmetic: complex128, NaN-propagating reductions and the
 // thread-group ("one group of n lanes per path") collectives.
 #pragma once
+#ifdef __CUDACC_RTC__
+// NVRTC (csrc JIT, paper_1804_03807_b200/jit.py): no host headers
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#define INFINITY __longlong_as_double(0x7ff0000000000000ULL)
+#define NAN __longlong_as_double(0x7ff8000000000000ULL)
+#define NID_NO_STD_HEADERS 1
+#else
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#endif
 
-#include "../../include/nid.h"
+#include "nid.h"
 
 #define NID_HD __host__ __device__ __forceinline__
 #define NID_D __device__ __forceinline__

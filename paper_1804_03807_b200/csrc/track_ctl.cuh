@@ -414,7 +414,33 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
 
 }  // namespace ctl
 
+// The default evaluator: the generic term-table interpreter (rows::eval_rows).
+// A JIT-compiled homotopy (csrc/jit_eval.h + paper_1804_03807_b200/jit.py)
+// supplies a policy with the same signature whose rows are straight-line code.
 template <int N>
+struct TableEval {
+  static NID_D void rows(const HomDev& H, int g, const cd (&x)[N], double t, const cd* prm, cd* aug, double* part,
+                         bool want_scale) {
+    rows::eval_rows<N>(H, g, x, t, prm, aug, part, want_scale);
+  }
+};
+
+// Optional phase timers (-DNID_PHASE_TIMERS): per-warp clock64 cycles spent
+// in each phase of the block loop, summed into TrackArgs::counters[8..15].
+#ifdef NID_PHASE_TIMERS
+#define NID_T0() long long t_ph_ = clock64()
+#define NID_TP(i)                                   \
+  do {                                              \
+    const long long t1_ = clock64();                \
+    if (lane == 0) ph_cyc[i] += (t1_ - t_ph_);      \
+    t_ph_ = t1_;                                    \
+  } while (0)
+#else
+#define NID_T0()
+#define NID_TP(i)
+#endif
+
+template <int N, class Eval = TableEval<N>>
 __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(const __grid_constant__ TrackArgs Ar) {
   using namespace ctl;
   using L = Lay<N>;
@@ -439,6 +465,9 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
   const SlotView V{cb + L::XE * S + cs, cb + L::XO * S + cs, cb + L::XS * S + cs, cb + L::DS * S + cs, db + cs,
                    ib + cs, lb + cs};
   unsigned long long n_eval = 0, n_jac = 0, n_scale = 0, n_fb = 0;
+#ifdef NID_PHASE_TIMERS
+  unsigned long long ph_cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
 #define W_IS(f) ib[(f) * S + lane]   // worker's slot
 #define W_DS(f) db[(f) * S + lane]
@@ -448,18 +477,23 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
   if (is_ctl) C_IS(I_ACT) = A_CLAIM;
 
   while (true) {
+    NID_T0();
     if (is_ctl) control<N>(Ar, V, nullptr);
+    NID_TP(0);  // control (top)
     // ------------------------------------------------------------ evaluation
     if (!__syncthreads_or(W_IS(I_ACT) != A_IDLE)) break;
+    NID_TP(1);  // barrier before the evaluation
     if (W_IS(I_ACT) == A_EVAL) {
       cd x[N];
 #pragma unroll
       for (int v = 0; v < N; ++v) x[v] = cb[(L::XE + v) * S + lane];
       const long long pr = lb[S + lane];
       const cd* prm = pr >= 0 ? Ar.params + pr : nullptr;
-      rows::eval_rows<N>(Ar.H, g, x, W_DS(D_TE), prm, aug, part, (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0);
+      Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0);
     }
+    NID_TP(2);  // evaluation
     __syncthreads();
+    NID_TP(3);  // barrier after the evaluation
     if (is_ctl && C_IS(I_ACT) == A_EVAL) {
       double sc = 0.0;
       const double r = rows::combine_resid<N>(augc, partc, C_DS(D_TE), sc);
@@ -485,6 +519,7 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
         control<N>(Ar, V, nullptr);
       }
     }
+    NID_TP(4);  // combine + control after the evaluation
     // ------------------------------------------------------------ LU (warp-local)
     // Warp g factorizes the CPW slots it controls: lane = q * CPW + sl (slot
     // sl, row group q; physical rows r == q (mod G)).  Slot-minor lanes keep
@@ -574,6 +609,7 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
       }
     }
     __syncwarp();
+    NID_TP(5);  // LU
     if (is_ctl && C_IS(I_ACT) == A_SOLVE) {  // back substitution by the slot's controller
       n_jac += 1;
       const unsigned long long pm = (unsigned long long)V.lsl[2 * S];
@@ -597,7 +633,12 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
         C_IS(I_ACT) = A_EVAL;  // re-evaluate the same point, then lstsq
       }
     }
+    NID_TP(6);  // back substitution + control
   }
+#ifdef NID_PHASE_TIMERS
+  if (lane == 0)
+    for (int i = 0; i < 7; ++i) atomicAdd(Ar.counters + 8 + i, ph_cyc[i]);
+#endif
 #undef W_IS
 #undef W_DS
 #undef C_IS

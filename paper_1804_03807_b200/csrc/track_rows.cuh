@@ -10,10 +10,15 @@
 namespace rows {
 
 constexpr int SLOTS = 32;  // paths per block
+#ifndef NID_G10
+#define NID_G10 4
+#endif
 
+// G: warps per block = threads per path (rows split G ways)
+NID_HD constexpr int groups_for(int n) { return n <= 3 ? 1 : (n <= 6 ? 2 : (n <= 10 ? NID_G10 : 8)); }
 template <int N>
-constexpr int groups() {  // G: warps per block = threads per path
-  return N <= 3 ? 1 : (N <= 6 ? 2 : (N <= 10 ? 4 : 8));
+constexpr int groups() {
+  return groups_for(N);
 }
 
 // shared-memory layout (complex units unless noted), each [item][slot]

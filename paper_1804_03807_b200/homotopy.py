@@ -157,6 +157,27 @@ class DeviceHomotopy:
     def n(self) -> int:
         return self.low.n
 
+    jit = False
+
+    def ensure_jit(self) -> None:
+        """Attach the NVRTC-specialised tracker (paper_1804_03807_b200/jit.py)."""
+        if not self.jit:
+            from . import jit as jitmod
+
+            jitmod.attach(self)
+
+
+# JIT heuristics: worth the ~4 s NVRTC compile for large launches of
+# moderately sized tables (huge tables make huge straight-line code)
+JIT_MIN_PATHS = 50_000
+JIT_MAX_TERMS = 1024
+
+
+def want_jit(dev: "DeviceHomotopy", paths: int, jit: bool | None) -> bool:
+    if jit is not None:
+        return bool(jit)
+    return paths >= JIT_MIN_PATHS and dev.low.nterms <= JIT_MAX_TERMS
+
 
 @dataclass(frozen=True)
 class LinearHomotopy:

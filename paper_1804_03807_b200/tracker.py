@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .homotopy import DeviceHomotopy, LinearHomotopy, TrackParams, lower, system_homotopy  # noqa: F401
+from .homotopy import DeviceHomotopy, LinearHomotopy, TrackParams, lower, system_homotopy, want_jit  # noqa: F401
 from .polys import PolySystem
 
 REGULAR = "regular"
@@ -123,7 +123,7 @@ _FOREIGN: dict = {}
 
 def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=None, first_index: int = 0,
                 count: int | None = None, target_params=None, param_div: int = 1,
-                out: TrackResults | None = None) -> TrackResults:
+                out: TrackResults | None = None, jit: bool | None = None) -> TrackResults:
     """Track many paths of h in one launch.
 
     starts: [P, n] start points, or None with `degrees` for total-degree
@@ -144,6 +144,8 @@ def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=
         P = int(count)
         deg = np.ascontiguousarray(degrees, dtype=np.int32)
     prm = None if target_params is None else np.ascontiguousarray(target_params, dtype=np.complex128)
+    if want_jit(dev, P, jit):
+        dev.ensure_jit()
     if out is None:  # (callers may pass preallocated, e.g. pinned, host arrays)
         out = TrackResults(np.empty((P, n), np.complex128), np.empty(P, np.int8), np.empty(P, np.int32),
                            np.empty(P, np.float64), np.empty(P, np.float64), np.empty(P, np.float64),
@@ -279,13 +281,16 @@ def classify(coords, n_original: int, infinity_threshold: float = 1e8, zero_tol:
 
 
 def track_batch_device(h, params: TrackParams, P: int, out: dict, *, degrees=None, first_index: int = 0,
-                       starts_ptr: int = 0, params_ptr: int = 0, param_div: int = 1, stream: int = 0) -> dict:
+                       starts_ptr: int = 0, params_ptr: int = 0, param_div: int = 1, stream: int = 0,
+                       jit: bool | None = None) -> dict:
     """Device-resident variant of `track_batch`: every buffer is a device
     pointer (e.g. torch CUDA tensors' data_ptr()), nothing is copied, and the
     kernels run on `stream`.  `out` maps x_end/status/steps/t_reached/
     residual/condition/regular to device pointers."""
     L = _lib.lib()
     dev = _device_of(h)
+    if want_jit(dev, P, jit):
+        dev.ensure_jit()
     deg = None if degrees is None else np.ascontiguousarray(degrees, dtype=np.int32)
     o = _lib.PathOutC(out["x_end"], out["status"], out["steps"], out["t_reached"], out["residual"],
                       out["condition"], out["regular"])

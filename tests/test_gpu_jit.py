@@ -1,0 +1,61 @@
+"""The NVRTC-specialised tracker (paper_1804_03807_b200/jit.py) against the
+reference's golden runs: same statuses, finite counts and endpoints as the
+table-driven kernel's parity tests demand (B200 only)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_1804_03807_b200 import configs, tracker
+from paper_1804_03807_b200.homotopy import LinearHomotopy
+from test_gpu_parity import compare_tracks
+
+pytestmark = pytest.mark.gpu
+
+
+def test_jit_c2_full(nid):
+    p = configs.c2()
+    fix = golden("track_c2")
+    res = tracker.track_batch(LinearHomotopy(p.start, p.target, p.gamma), None, degrees=p.degrees,
+                              count=p.paths, jit=True)
+    compare_tracks(res, fix, 0.99)
+
+
+def test_jit_c5_sample(nid):
+    p = configs.c5()
+    fix = golden("track_c5_sample")
+    res = tracker.track_batch(LinearHomotopy(p.start, p.target, p.gamma), fix["starts"], jit=True)
+    compare_tracks(res, fix, 0.97)
+
+
+def test_jit_c1_and_general_homotopy(nid):
+    """quadrics (exponent 2) and a generic (merged-table) start system"""
+    p = configs.c1()
+    fix = golden("track_c1")
+    res = tracker.track_batch(LinearHomotopy(p.start, p.target, p.gamma), fix["starts"], jit=True)
+    compare_tracks(res, fix, 1.0)
+    # cascade-style homotopy (start != total degree, shared rows): JIT vs table kernel
+    from paper_1804_03807_b200 import cascade
+    pd = configs.c3_mini()
+    h = cascade._slack_removal_homotopy(pd.emb, 0.6 + 0.8j)
+    g = golden("pipeline_c3m")
+    starts = g["L2_nonzero_x"][:32]
+    a = tracker.track_batch(h, starts, jit=False)
+    h2 = cascade._slack_removal_homotopy(pd.emb, 0.6 + 0.8j)
+    b = tracker.track_batch(h2, starts, jit=True)
+    assert np.array_equal(a.status, b.status)
+    ok = a.succeeded
+    assert np.max(np.abs(a.x[ok] - b.x[ok])) < 1e-8
+
+
+def test_jit_membership_params(nid):
+    """per-path target coefficients through the JIT evaluator"""
+    from paper_1804_03807_b200 import filtering
+    from paper_1804_03807_b200.tracker import Solution
+    g = golden("membership_c3m")
+    pd = configs.c3_mini()
+    w = filtering.WitnessSet(2, pd.emb, [Solution(x, 0.0, 1.0) for x in g["witness"]])
+    mh = filtering.MembershipHomotopy(w)
+    mh.dev.ensure_jit()
+    verdict, _ = filtering.membership_batch(w, g["candidates"], mh=mh)
+    assert list(verdict) == list(g["verdict"])
