@@ -515,8 +515,27 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
         n_scale += (C_IS(I_FLAGS) & F_NEEDSCALE) ? 1 : 0;
         C_DS(D_RESID) = r;
         C_DS(D_SCALE) = sc;
-        C_IS(I_ACT) = A_ON_EVAL;
-        control<N>(Ar, V, nullptr);
+        // inline fast path of the commonest transition: the corrector's
+        // residual is above its tolerance -> Newton step (tracker.py:194-199)
+        bool fast = false;
+        const int ph = C_IS(I_CPHASE);
+        if (C_IS(I_MODE) == M_CORR && ph != 2 && !(ph == 0 && C_IS(I_CITERS) == 0) && isfinite(r)) {
+          double tol_eff;
+          if (ph == 0) {
+            tol_eff = fmax(C_DS(D_CTOL), NOISE_ULPS * sc);
+            C_DS(D_CTOLEFF) = tol_eff;
+          } else {
+            tol_eff = C_DS(D_CTOLEFF);
+          }
+          if (!(r <= tol_eff)) {
+            C_IS(I_ACT) = A_SOLVE;
+            fast = true;
+          }
+        }
+        if (!fast) {
+          C_IS(I_ACT) = A_ON_EVAL;
+          control<N>(Ar, V, nullptr);
+        }
       }
     }
     NID_TP(4);  // combine + control after the evaluation
@@ -584,6 +603,16 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
             for (int r = q; r < N; r += G) {
               const int pos = (pinv >> (4 * r)) & 15;
               if (pos > k) {
+#ifdef NID_LU_FMA
+                const cd l = A<N>(augs, r, k) * inv;
+#pragma unroll
+                for (int j = 1; j <= N; ++j) {
+                  if (j > k) {
+                    cd& a = A<N>(augs, r, j);
+                    a = cfms(a, l, prow[j]);
+                  }
+                }
+#else
                 const cd l = cmul_nf(A<N>(augs, r, k), inv);
 #pragma unroll
                 for (int j = 1; j <= N; ++j) {
@@ -592,6 +621,7 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
                     a = csub_nf(a, cmul_nf(l, prow[j]));
                   }
                 }
+#endif
               }
             }
             __syncwarp();
@@ -625,8 +655,32 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
         fin = fin && cfinite(dx[k]);
       }
       if (!C_IS(I_BAD) && fin) {
-        C_IS(I_ACT) = A_ON_SOLVE;
-        control<N>(Ar, V, dx);
+        bool fast = false;
+        if (C_IS(I_MODE) == M_CORR) {  // inline: x += dx, next corrector evaluation (tracker.py:200-205)
+          bool xfin = true;
+          cd xn[N];
+#pragma unroll
+          for (int v = 0; v < N; ++v) {
+            xn[v] = V.xes[v * S] + dx[v];
+            xfin = xfin && cfinite(xn[v]);
+          }
+          if (xfin) {
+#pragma unroll
+            for (int v = 0; v < N; ++v) V.xes[v * S] = xn[v];
+            const int it = C_IS(I_CIT) + 1;
+            C_IS(I_CIT) = it;
+            const int ph = (it >= C_IS(I_CITERS)) ? 2 : 1;
+            C_IS(I_CPHASE) = ph;
+            if (ph == 2) C_IS(I_FLAGS) |= F_NEEDSCALE;
+            else C_IS(I_FLAGS) &= ~F_NEEDSCALE;
+            C_IS(I_ACT) = A_EVAL;
+            fast = true;
+          }
+        }
+        if (!fast) {
+          C_IS(I_ACT) = A_ON_SOLVE;
+          control<N>(Ar, V, dx);
+        }
       } else {
         n_fb += 1;
         C_IS(I_FLAGS) |= F_FALLBACK;

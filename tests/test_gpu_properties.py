@@ -1,0 +1,60 @@
+"""Size-independent properties at full BASELINE sizes, and multiplicity
+known answers (B200 only)."""
+
+import numpy as np
+import pytest
+
+from oracle import nid_oracle as O
+from paper_1804_03807_b200 import configs, filtering, tracker
+from paper_1804_03807_b200.homotopy import LinearHomotopy
+from paper_1804_03807_b200.polys import PolySystem, make_poly
+from paper_1804_03807_b200.systems import total_degree_start, total_degree_starts
+from paper_1804_03807_b200.tracker import Solution
+
+pytestmark = pytest.mark.gpu
+
+C5_MIXED_VOLUME = 35940  # reference polyhedral.mixed_volume(cyclic_support(10))
+
+
+def test_c5_full_scale_properties(nid):
+    """All 3,628,800 C5 paths: finite endpoints are roots (residual <= 1e-8),
+    pairwise distinct, and no more than the mixed volume."""
+    p = configs.c5()
+    h = LinearHomotopy(p.start, p.target, p.gamma)
+    res = tracker.track_batch(h, None, degrees=p.degrees, count=p.paths)
+    fin = res.succeeded
+    nf = int(fin.sum())
+    assert 0.6 * C5_MIXED_VOLUME < nf <= C5_MIXED_VOLUME
+    assert np.all(res.residual[fin] <= 1e-8)
+    X = res.x[fin]
+    Hv, _, _ = LinearHomotopy(p.target, p.target).evaluate(X, np.ones(len(X)))
+    assert np.max(np.abs(Hv)) <= 1e-8
+    pairs = filtering.match_pairs(X)
+    assert len(pairs) == 0  # distinct roots: every finite path found a different one
+    assert set(np.unique(res.status)) <= {0, 1, 2, 3}
+
+
+def eq6():
+    # (x1-1)(x1-2) = 0, (x1-1) x2^2 = 0: a line x1 = 1 and the double point (2, 0)
+    return PolySystem(2, (make_poly(2, [((2, 0), 1), ((1, 0), -3), ((0, 0), 2)]),
+                          make_poly(2, [((1, 2), 1), ((0, 2), -1)])))
+
+
+def test_multiplicity_of_double_point_matches_oracle(nid):
+    f = eq6()
+    g = total_degree_start(f)
+    gamma = 0.6 + 0.8j
+    starts = total_degree_starts(f.degrees())
+    gpu = tracker.track_batch(LinearHomotopy(g, f, gamma), starts)
+    h = O.LinearHomotopy(g, f, gamma)
+    ref = [O.track(h, s) for s in starts]
+    assert [tracker.STATUS_NAMES[int(s)] for s in gpu.status] == [r.status for r in ref]
+    # endpoints near (2, 0): the double point, reached by two paths -> multiplicity 2
+    pts = [Solution(gpu.x[i], float(gpu.residual[i]), 1.0) for i in range(len(starts))
+           if gpu.succeeded[i] and abs(gpu.x[i][0] - 2) < 1e-3]
+    rpts = [O.Solution(r.endpoint.coordinates, r.endpoint.residual, 1.0) for r in ref
+            if r.succeeded and abs(r.endpoint.coordinates[0] - 2) < 1e-3]
+    kept, mult = filtering.dedup(pts)
+    rkept, rmult = O.dedup(rpts)
+    assert sorted(mult) == sorted(rmult)
+    assert len(pts) == len(rpts)
