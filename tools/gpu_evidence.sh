@@ -11,4 +11,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python tools/probe_c5.py 200000 > gpurun_out/plain_probe.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:track_ctl -c 1 -o gpurun_out/prof_track_r01 \
   python tools/probe_c5.py 200000 > gpurun_out/ncu_full.log 2>&1
-tail -2 gpurun_out/ref_arm.log gpurun_out/torchrun1.log gpurun_out/ncu_launches.log gpurun_out/ncu_full.log
+tail -n 2 gpurun_out/ref_arm.log gpurun_out/torchrun1.log gpurun_out/ncu_launches.log gpurun_out/ncu_full.log
