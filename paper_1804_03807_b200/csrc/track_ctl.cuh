@@ -552,27 +552,27 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
       cd* const augs = cb + ss;
       const bool solving = ib[I_ACT * S + ss] == A_SOLVE;
       if (__any_sync(0xffffffffu, solving)) {
-        unsigned long long perm = 0, pinv = 0;
+        // Column-split LU over the slot's G lanes: logical row order is an
+        // implicit permutation (perm: position -> physical row, swapped
+        // exactly as zgetf2 swaps rows), so every lane runs the same row loop
+        // (uniform trip count N-1-k) and owns columns j == k+1+q (mod G).
+        unsigned long long perm = 0;
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          perm |= (unsigned long long)i << (4 * i);
-          pinv |= (unsigned long long)i << (4 * i);
-        }
+        for (int i = 0; i < N; ++i) perm |= (unsigned long long)i << (4 * i);
         bool bad = false;
 #pragma unroll 1
         for (int k = 0; k < N; ++k) {
           double best = -1.0;
           int bpos = N;
-          if (solving) {
 #pragma unroll
-            for (int r = q; r < N; r += G) {
-              const int pos = (pinv >> (4 * r)) & 15;
-              if (pos >= k) {
-                const double key = cabs1(A<N>(augs, r, k));
-                if (key > best || (key == best && pos < bpos)) {
-                  best = key;
-                  bpos = pos;
-                }
+          for (int m = 0; m < (N + G - 1) / G; ++m) {
+            const int pos = k + q + m * G;
+            if (pos < N) {
+              const int r = (perm >> (4 * pos)) & 15;
+              const double key = cabs1(A<N>(augs, r, k));
+              if (key > best) {  // positions ascend with m: first max wins ties
+                best = key;
+                bpos = pos;
               }
             }
           }
@@ -585,52 +585,46 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
               bpos = op;
             }
           }
+          const int pk = bpos < N ? bpos : k;
+          if (!(best > 0.0)) bad = true;
+          const unsigned long long rk = (perm >> (4 * k)) & 15, rp = (perm >> (4 * pk)) & 15;
+          perm &= ~((15ull << (4 * k)) | (15ull << (4 * pk)));
+          perm |= (rp << (4 * k)) | (rk << (4 * pk));
+          const int r0 = (int)rp;
+          const cd inv = crecip_fast(A<N>(augs, r0, k));
+          constexpr int MC = (N + G - 1) / G;  // most columns a lane owns
+          cd prow[MC];
+#pragma unroll
+          for (int m = 0; m < MC; ++m) {
+            const int j = k + 1 + q + m * G;
+            if (j <= N) prow[m] = A<N>(augs, r0, j);
+          }
           if (solving) {
-            const int pk = bpos < N ? bpos : k;
-            if (!(best > 0.0)) bad = true;
-            const unsigned long long rk = (perm >> (4 * k)) & 15, rp = (perm >> (4 * pk)) & 15;
-            perm &= ~((15ull << (4 * k)) | (15ull << (4 * pk)));
-            perm |= (rp << (4 * k)) | (rk << (4 * pk));
-            pinv &= ~((15ull << (4 * rk)) | (15ull << (4 * rp)));
-            pinv |= ((unsigned long long)k << (4 * rp)) | ((unsigned long long)pk << (4 * rk));
-            const int r0 = (int)rp;
-            cd prow[N + 1];
-#pragma unroll
-            for (int j = 1; j <= N; ++j)
-              if (j > k) prow[j] = A<N>(augs, r0, j);
-            const cd inv = crecip_fast(A<N>(augs, r0, k));
 #pragma unroll 1
-            for (int r = q; r < N; r += G) {
-              const int pos = (pinv >> (4 * r)) & 15;
-              if (pos > k) {
+            for (int pos = k + 1; pos < N; ++pos) {
+              const int r = (perm >> (4 * pos)) & 15;
 #ifdef NID_LU_FMA
-                const cd l = A<N>(augs, r, k) * inv;
-#pragma unroll
-                for (int j = 1; j <= N; ++j) {
-                  if (j > k) {
-                    cd& a = A<N>(augs, r, j);
-                    a = cfms(a, l, prow[j]);
-                  }
-                }
+              const cd l = A<N>(augs, r, k) * inv;
 #else
-                const cd l = cmul_nf(A<N>(augs, r, k), inv);
-#pragma unroll
-                for (int j = 1; j <= N; ++j) {
-                  if (j > k) {
-                    cd& a = A<N>(augs, r, j);
-                    a = csub_nf(a, cmul_nf(l, prow[j]));
-                  }
-                }
+              const cd l = cmul_nf(A<N>(augs, r, k), inv);
 #endif
+#pragma unroll
+              for (int m = 0; m < MC; ++m) {
+                const int j = k + 1 + q + m * G;
+                if (j <= N) {
+                  cd& a = A<N>(augs, r, j);
+#ifdef NID_LU_FMA
+                  a = cfms(a, l, prow[m]);
+#else
+                  a = csub_nf(a, cmul_nf(l, prow[m]));
+#endif
+                }
               }
             }
-            __syncwarp();
-            // the pivot's reciprocal replaces it (the back substitution multiplies)
-            if (q == r0 % G) A<N>(augs, r0, k) = inv;
-          } else {
-            __syncwarp();
           }
           __syncwarp();
+          // the pivot's reciprocal replaces it (the back substitution multiplies)
+          if (solving && q == 0) A<N>(augs, r0, k) = inv;
         }
         if (solving && q == 0) {
           lb[2 * S + ss] = (long long)perm;
