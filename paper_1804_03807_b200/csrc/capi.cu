@@ -42,6 +42,7 @@ struct NidHomotopy {
   cd gamma;
   int* row_off;
   uint4* expo;
+  uint4 *fac, *fex;
   cd *cs, *ct;
   double *acs, *act;
   int8_t* pslot;
@@ -60,6 +61,8 @@ struct NidHomotopy {
     for (int v = 0; v <= 16; ++v) h.goff[v] = goff[v];
     h.row_off = row_off;
     h.expo = expo;
+    h.fac = fac;
+    h.fex = fex;
     h.cs = cs;
     h.ct = ct;
     h.acs = acs;
@@ -236,6 +239,8 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   cudaError_t e = cudaSuccess;
   e = e ? e : cudaMalloc(&h->row_off, (n + 1) * sizeof(int));
   e = e ? e : cudaMalloc(&h->expo, Tp * sizeof(uint4));
+  e = e ? e : cudaMalloc(&h->fac, Tp * sizeof(uint4));
+  e = e ? e : cudaMalloc(&h->fex, Tp * sizeof(uint4));
   e = e ? e : cudaMalloc(&h->cs, Tp * sizeof(cd));
   e = e ? e : cudaMalloc(&h->ct, Tp * sizeof(cd));
   e = e ? e : cudaMalloc(&h->acs, Tp * sizeof(double));
@@ -244,6 +249,27 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   if (!e && d->param_slot) e = cudaMalloc(&h->pslot, Tp);
   if (!e) e = cudaMemcpy(h->row_off, off.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice);
   if (!e && T) e = cudaMemcpy(h->expo, d->expo, T * sizeof(uint4), cudaMemcpyHostToDevice);
+  if (!e && T) {
+    // factor lists of every term (the tracker's evaluator loops over the
+    // variables a term contains instead of over all n)
+    std::vector<uint4> fac(T), fex(T);
+    for (int k = 0; k < T; ++k) {
+      unsigned long long vl = 0;
+      unsigned ex[4] = {0, 0, 0, 0};
+      int nf = 0;
+      for (int v = 0; v < n; ++v) {
+        const int a = d->expo[k * NID_MAX_VARS + v];
+        if (!a) continue;
+        vl |= (unsigned long long)v << (4 * nf);
+        ex[nf >> 2] |= (unsigned)a << (8 * (nf & 3));
+        ++nf;
+      }
+      fac[k] = make_uint4((unsigned)vl, (unsigned)(vl >> 32), (unsigned)nf, 0u);
+      fex[k] = make_uint4(ex[0], ex[1], ex[2], ex[3]);
+    }
+    e = cudaMemcpy(h->fac, fac.data(), T * sizeof(uint4), cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(h->fex, fex.data(), T * sizeof(uint4), cudaMemcpyHostToDevice);
+  }
   if (!e && T) e = cudaMemcpy(h->cs, d->coef_start, T * sizeof(cd), cudaMemcpyHostToDevice);
   if (!e && T) e = cudaMemcpy(h->ct, d->coef_target, T * sizeof(cd), cudaMemcpyHostToDevice);
   if (!e && T) e = cudaMemcpy(h->acs, acs.data(), T * sizeof(double), cudaMemcpyHostToDevice);
@@ -311,6 +337,8 @@ int nid_homotopy_destroy(NidHomotopy* h) {
   if (h->jit_lib) cudaLibraryUnload(h->jit_lib);
   cudaFree(h->row_off);
   cudaFree(h->expo);
+  cudaFree(h->fac);
+  cudaFree(h->fex);
   cudaFree(h->cs);
   cudaFree(h->ct);
   cudaFree(h->acs);

@@ -32,6 +32,10 @@ struct HomDev {
   int goff[17];
   const int* row_off;     // [n+1]
   const uint4* expo;      // [nterms], 16 exponent bytes
+  // factor lists (tracker evaluator): x,y = indices of the term's variables,
+  // ascending, 4 bits each; z = their count.  fex: their exponents, 8 bits each
+  const uint4* fac;
+  const uint4* fex;
   const cd* cs;           // start coefficients
   const cd* ct;           // target coefficients
   const double* acs;      // |cs|

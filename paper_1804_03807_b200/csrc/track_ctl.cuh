@@ -58,7 +58,8 @@ struct Lay {
   // doubles [item][slot]: slot state + per-group partial maxima / pivot exchange
   static constexpr int DST = 0;
   static constexpr int PART = D_COUNT;       // 3*G: r2, sS, sT per group (reused for pivot key/pos)
-  static constexpr int DBL = PART + 3 * G;
+  static constexpr int AXW = PART + 3 * G;   // G*N: each warp's |x_v| scratch (evaluator)
+  static constexpr int DBL = AXW + G * N;
   // long long [item][slot]: path index, parameter row, LU row permutation
   static constexpr int LLN = 3;
   static constexpr size_t bytes() {
@@ -420,8 +421,12 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
 template <int N>
 struct TableEval {
   static NID_D void rows(const HomDev& H, int g, const cd (&x)[N], double t, const cd* prm, cd* aug, double* part,
-                         bool want_scale) {
+                         bool want_scale, const cd* xs, double* axw) {
+#ifdef NID_EVAL_DENSE
     rows::eval_rows<N>(H, g, x, t, prm, aug, part, want_scale);
+#else
+    rows::eval_rows_fac<N>(H, g, xs, t, prm, aug, part, want_scale, axw);
+#endif
   }
 };
 
@@ -489,7 +494,8 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
       for (int v = 0; v < N; ++v) x[v] = cb[(L::XE + v) * S + lane];
       const long long pr = lb[S + lane];
       const cd* prm = pr >= 0 ? Ar.params + pr : nullptr;
-      Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0);
+      Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0,
+                 cb + L::XE * S + lane, db + (L::AXW + g * N) * S + lane);
     }
     NID_TP(2);  // evaluation
     __syncthreads();

@@ -188,6 +188,155 @@ NID_D void eval_rows(const HomDev& H, int g, const cd (&x)[N], double t, const c
   dbl[(L::ST + g) * SLOTS] = mT;
 }
 
+// ---------------------------------------------------------------------------
+// Factor-list evaluator (the tracker's default): a term loops over the K
+// variables it contains (K = its factor count, dispatched to a fully
+// unrolled body per K) instead of over all n with predicated bodies; the
+// point is read from the slot's shared-memory copy and the Jacobian row is
+// accumulated in place in the augmented matrix.  The arithmetic -- prefix
+// products in ascending variable order, one suffix pass for the partials,
+// abs-sum scale -- is operation for operation that of `term` above.
+template <int N, int K, bool ML>
+NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const double* axs, bool ws, cd c, cd* row,
+                 cd& hv, double& m) {
+  // only the prefix products stay live between the passes: indices,
+  // exponents and x are re-read (shared memory / the term's words)
+  cd P[K];
+  uint4 fe = make_uint4(0u, 0u, 0u, 0u);
+  if (!ML) fe = __ldg(H.fex + k);
+  cd p = cd{1.0, 0.0};
+  m = 1.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int v = ((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15;
+    const cd x = xs[v * SLOTS];
+    P[j] = p;
+    if (ML) {
+      p = p * x;
+      if (ws) m = __dmul_rn(m, axs[v * SLOTS]);
+    } else {
+      const int a = ((j < 4 ? fe.x : (j < 8 ? fe.y : (j < 12 ? fe.z : fe.w))) >> (8 * (j & 3))) & 255;
+      p = p * (a == 1 ? x : upow(x, a));
+      if (ws) {
+        const double ax = axs[v * SLOTS];
+        double pv = ax;
+#pragma unroll 1
+        for (int e = 1; e < a; ++e) pv = __dmul_rn(pv, ax);
+        m = __dmul_rn(m, pv);
+      }
+    }
+  }
+  hv = cfma(c, p, hv);
+  cd s = c;
+#pragma unroll
+  for (int j = K - 1; j >= 0; --j) {
+    const int v = ((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15;
+    const cd x = xs[v * SLOTS];
+    cd* const J = row + v * SLOTS;
+    if (ML) {
+      *J = cfma(P[j], s, *J);
+      s = s * x;
+    } else {
+      const int a = ((j < 4 ? fe.x : (j < 8 ? fe.y : (j < 12 ? fe.z : fe.w))) >> (8 * (j & 3))) & 255;
+      if (a == 1) {
+        *J = cfma(P[j], s, *J);
+        s = s * x;
+      } else {
+        const cd q = upow(x, a - 1);
+        *J = cfma(P[j] * ((double)a * q), s, *J);
+        s = s * (q * x);
+      }
+    }
+  }
+}
+
+template <int N, bool ML>
+NID_D void fterm_dispatch(const HomDev& H, int k, const uint4 f, const cd* xs, const double* axs, bool ws, cd c,
+                          cd* row, cd& hv, double& m) {
+  switch (f.z) {
+#define NID_FT(KK) \
+  case KK:         \
+    if (KK <= N) fterm<N, (KK <= N ? KK : 1), ML>(H, k, f, xs, axs, ws, c, row, hv, m); \
+    break;
+    NID_FT(1) NID_FT(2) NID_FT(3) NID_FT(4) NID_FT(5) NID_FT(6) NID_FT(7) NID_FT(8)
+    NID_FT(9) NID_FT(10) NID_FT(11) NID_FT(12) NID_FT(13) NID_FT(14) NID_FT(15) NID_FT(16)
+#undef NID_FT
+    default:  // constant term
+      hv = cfma(c, cd{1.0, 0.0}, hv);
+      m = 1.0;
+  }
+}
+
+// Rows of warp group g into the slot's augmented matrix (as eval_rows).
+// xs: the slot's evaluation point in shared memory (stride SLOTS); axw: this
+// warp's |x_v| scratch for the slot.
+template <int N>
+NID_D void eval_rows_fac(const HomDev& H, int g, const cd* xs, double t, const cd* prm, cd* aug, double* dbl,
+                         bool want_scale, double* axw) {
+  using L = Layout<N>;
+  const cd alpha = (1.0 - t) * H.gamma;
+  const bool ws = __any_sync(__activemask(), want_scale);
+  if (ws) {
+#pragma unroll
+    for (int v = 0; v < N; ++v) axw[v * SLOTS] = cabs_fast(xs[v * SLOTS]);
+  }
+  double r2 = 0.0, mS = 0.0, mT = 0.0;
+#pragma unroll 1
+  for (int gi = H.goff[g]; gi < H.goff[g + 1]; ++gi) {
+    const int i = H.grow[gi];
+    cd* const row = aug + i * (N + 1) * SLOTS;
+#pragma unroll
+    for (int v = 0; v < N; ++v) row[v * SLOTS] = cd{0.0, 0.0};
+    cd hv = cd{0.0, 0.0};
+    const int k0 = __ldg(H.row_off + i), k1 = __ldg(H.row_off + i + 1);
+    double sS = 0.0, sT = 0.0;
+#pragma unroll 1
+    for (int k = k0; k < k1; ++k) {
+      const uint4 f = __ldg(H.fac + k);
+      cd ct = ldg_c(H.ct + k);
+      if (H.pslot != nullptr) {
+        const int sl = __ldg(H.pslot + k);
+        if (sl >= 0) ct = prm[sl];
+      }
+      const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
+      double m;
+      if (H.multilinear) {
+        fterm_dispatch<N, true>(H, k, f, xs, axw, ws, c, row, hv, m);
+      } else {
+        fterm_dispatch<N, false>(H, k, f, xs, axw, ws, c, row, hv, m);
+      }
+      if (ws) {
+        if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
+        sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), m));
+      }
+    }
+    if (H.td) {  // G_i = x_i^{d_i} - 1 in closed form
+      const int d = H.tddeg[i];
+      const cd xi = xs[i * SLOTS];
+      cd q = cd{1.0, 0.0};
+#pragma unroll 1
+      for (int e = 1; e < d; ++e) q = q * xi;
+      hv = cfma(alpha, q * xi - cd{1.0, 0.0}, hv);
+      const cd dj = alpha * ((double)d * q);
+      row[i * SLOTS] = row[i * SLOTS] + dj;
+      if (ws) {
+        const double axi = axw[i * SLOTS];
+        double m = 1.0;
+#pragma unroll 1
+        for (int e = 0; e < d; ++e) m = __dmul_rn(m, axi);
+        sS = __dadd_rn(1.0, m);
+      }
+    }
+    row[N * SLOTS] = -hv;
+    r2 = nanmax(r2, cabs2(hv));
+    mS = fmax(mS, sS);
+    mT = fmax(mT, sT);
+  }
+  dbl[(L::R2 + g) * SLOTS] = r2;
+  dbl[(L::SS + g) * SLOTS] = mS;
+  dbl[(L::ST + g) * SLOTS] = mT;
+}
+
 // combine the G partial maxima (after a barrier): residual max|H_i| and scale
 template <int N>
 NID_D double combine_resid(const cd* aug, const double* dbl, double t, double& scale) {
