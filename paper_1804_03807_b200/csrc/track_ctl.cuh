@@ -58,8 +58,10 @@ struct Lay {
   // doubles [item][slot]: slot state + per-group partial maxima / pivot exchange
   static constexpr int DST = 0;
   static constexpr int PART = D_COUNT;       // 3*G: r2, sS, sT per group (reused for pivot key/pos)
-  static constexpr int AXW = PART + 3 * G;   // G*N: each warp's |x_v| scratch (evaluator)
-  static constexpr int DBL = AXW + G * N;
+  // N: |x_v| of the evaluation point (evaluator scratch; every warp writes
+  // the same values for its lane's slot before reading them)
+  static constexpr int AXW = PART + 3 * G;
+  static constexpr int DBL = AXW + N;
   // long long [item][slot]: path index, parameter row, LU row permutation
   static constexpr int LLN = 3;
   static constexpr size_t bytes() {
@@ -87,11 +89,19 @@ struct SlotView {
 #define SETF(fl, on) (IS_(I_FLAGS) = (on) ? (IS_(I_FLAGS) | (fl)) : (IS_(I_FLAGS) & ~(fl)))
 
 // The controller: runs slot transitions until the slot needs an evaluation
-// or a solve, or goes idle.  dxv: the Newton step just solved (A_ON_SOLVE).
-// Not inlined: one copy of the state machine in the binary.
+// or a solve, or goes idle.  dxv: the Newton step just solved (A_ON_SOLVE),
+// left by the back substitution in the augmented matrix's last column
+// (stride (N+1)*SLOTS).  Called from one site only (the top of the block
+// loop), so inlining it costs no code duplication.
+#ifdef NID_CTL_NOINLINE
+#define NID_CTL_ATTR __noinline__
+#else
+#define NID_CTL_ATTR __forceinline__
+#endif
 template <int N>
-__device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, const cd* dxv) {
+__device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, const cd* dxv) {
   constexpr int S = SLOTS;
+  constexpr int DXST = (N + 1) * SLOTS;
   const NidTrackParams& q = Ar.prm;
   cd* const xes = V.xes;
   cd* const xos = V.xos;
@@ -184,7 +194,7 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
         if (IS_(I_MODE) == M_CORR) {
           bool fin = true;
           for (int v = 0; v < N; ++v) {
-            const cd x = xes[v * S] + dxv[v];
+            const cd x = xes[v * S] + dxv[v * DXST];
             xes[v * S] = x;
             fin = fin && cfinite(x);
           }
@@ -203,8 +213,8 @@ __device__ __noinline__ void control(const TrackArgs& Ar, const SlotView& V, con
         DS_(D_DNLAM) = 1.0;
         IS_(I_DNTRIAL) = 0;
         for (int v = 0; v < N; ++v) {
-          dss[v * S] = dxv[v];
-          xes[v * S] = xss[v * S] + dxv[v];
+          dss[v * S] = dxv[v * DXST];
+          xes[v * S] = xss[v * S] + dxv[v * DXST];
         }
         act = A_EVAL;
         break;
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
 
   while (true) {
     NID_T0();
-    if (is_ctl) control<N>(Ar, V, nullptr);
+    if (is_ctl) control<N>(Ar, V, augc + N * S);
     NID_TP(0);  // control (top)
     // ------------------------------------------------------------ evaluation
     if (!__syncthreads_or(W_IS(I_ACT) != A_IDLE)) break;
@@ -495,7 +505,7 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
       const long long pr = lb[S + lane];
       const cd* prm = pr >= 0 ? Ar.params + pr : nullptr;
       Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0,
-                 cb + L::XE * S + lane, db + (L::AXW + g * N) * S + lane);
+                 cb + L::XE * S + lane, db + L::AXW * S + lane);
     }
     NID_TP(2);  // evaluation
     __syncthreads();
@@ -514,8 +524,8 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
         }
         double sv[N];
         lstsq_minnorm(sc2, N, N, N, sc2 + N * N, sc2 + N * N + N, sv, sc2 + 2 * N * N + N);
-        C_IS(I_ACT) = A_ON_SOLVE;
-        control<N>(Ar, V, sc2 + 2 * N * N + N);
+        for (int i = 0; i < N; ++i) A<N>(augc, i, N) = sc2[2 * N * N + N + i];
+        C_IS(I_ACT) = A_ON_SOLVE;  // consumed by the next control round
       } else {
         n_eval += 1;
         n_scale += (C_IS(I_FLAGS) & F_NEEDSCALE) ? 1 : 0;
@@ -538,10 +548,7 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
             fast = true;
           }
         }
-        if (!fast) {
-          C_IS(I_ACT) = A_ON_EVAL;
-          control<N>(Ar, V, nullptr);
-        }
+        if (!fast) C_IS(I_ACT) = A_ON_EVAL;  // consumed by the next control round
       }
     }
     NID_TP(4);  // combine + control after the evaluation
@@ -678,8 +685,9 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
           }
         }
         if (!fast) {
-          C_IS(I_ACT) = A_ON_SOLVE;
-          control<N>(Ar, V, dx);
+#pragma unroll
+          for (int v = 0; v < N; ++v) A<N>(augc, v, N) = dx[v];
+          C_IS(I_ACT) = A_ON_SOLVE;  // consumed by the next control round
         }
       } else {
         n_fb += 1;
