@@ -365,7 +365,7 @@ int nid_last_counters(NidCounters* c) {
 // slot map for the workspace cache
 enum {
   W_STARTS = 0, W_PARAMS, W_XEND, W_STATUS, W_STEPS, W_TREACH, W_RESID, W_COND, W_REG,
-  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS
+  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS, W_GSTATE
 };
 
 int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
@@ -463,6 +463,8 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
   const int max_blocks = sm_count() * 8;
   a.scratch = ws<cd>(W_SCR, (size_t)max_blocks * k_tthreads[n]() * (3 * n * n + 2 * n));
   if (!a.scratch) FAIL("out of device memory (scratch)");
+  a.gstate = ws<cd>(W_GSTATE, (size_t)max_blocks * 3 * n * rows::SLOTS);
+  if (!a.gstate) FAIL("out of device memory (slot state)");
 
   cudaEvent_t e0, e1, e2;
   CK(cudaEventCreate(&e0));

@@ -23,6 +23,7 @@ struct TrackArgs {
   double* resid;
   unsigned long long* counters;  // evals, jacs, scales, lstsq fallbacks
   cd* scratch;                   // per-group lstsq scratch, 3*n*n + 2*n complex each
+  cd* gstate;                    // per-slot accepted/previous point, DN direction [block][3n][32]
 };
 
 // control actions

@@ -51,10 +51,11 @@ struct Lay {
   // complex [item][slot]
   static constexpr int AUG = 0;              // N*(N+1) augmented matrix
   static constexpr int XE = N * (N + 1);     // evaluation point
-  static constexpr int XO = XE + N;          // accepted point
-  static constexpr int XS = XO + N;          // x_prev / damped-Newton base
-  static constexpr int DS = XS + N;          // damped-Newton direction
-  static constexpr int CPLX = DS + N;
+  static constexpr int CPLX = XE + N;
+  // the accepted point, x_prev / damped-Newton base and damped-Newton
+  // direction (touched once per step, not per Newton iteration) live in
+  // global memory, [block][item][slot] (TrackArgs::gstate): 3 blocks per SM
+  static constexpr int GXO = 0, GXS = N, GDS = 2 * N, GITEMS = 3 * N;
   // doubles [item][slot]: slot state + per-group partial maxima / pivot exchange
   static constexpr int DST = 0;
   static constexpr int PART = D_COUNT;       // 3*G: r2, sS, sT per group (reused for pivot key/pos)
@@ -69,6 +70,15 @@ struct Lay {
                             I_COUNT * sizeof(int));
   }
 };
+
+// blocks per SM the register budget is sized for: as many as the shared
+// memory admits (228 KB per SM, 1 KB reserved per block), at most 3
+template <int N>
+constexpr int min_blocks() {
+  constexpr int fit = (int)((228u * 1024u) / (Lay<N>::bytes() + 1024u));
+  constexpr int cap = Lay<N>::G <= 4 ? 3 : 2;
+  return fit < 1 ? 1 : (fit > cap ? cap : fit);
+}
 
 }  // namespace ctl
 
@@ -456,7 +466,7 @@ struct TableEval {
 #endif
 
 template <int N, class Eval = TableEval<N>>
-__global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(const __grid_constant__ TrackArgs Ar) {
+__global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>()) track_ctl_kernel(const __grid_constant__ TrackArgs Ar) {
   using namespace ctl;
   using L = Lay<N>;
   constexpr int G = L::G;
@@ -477,7 +487,8 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, 2) track_ctl_kernel(co
   const int cs = g * CPW + (lane % CPW);
   cd* const augc = cb + cs;
   double* const partc = db + L::PART * S + cs;
-  const SlotView V{cb + L::XE * S + cs, cb + L::XO * S + cs, cb + L::XS * S + cs, cb + L::DS * S + cs, db + cs,
+  cd* const gs = Ar.gstate + (size_t)blockIdx.x * L::GITEMS * S + cs;
+  const SlotView V{cb + L::XE * S + cs, gs + L::GXO * S, gs + L::GXS * S, gs + L::GDS * S, db + cs,
                    ib + cs, lb + cs};
   unsigned long long n_eval = 0, n_jac = 0, n_scale = 0, n_fb = 0;
 #ifdef NID_PHASE_TIMERS
