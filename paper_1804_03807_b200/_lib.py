@@ -12,7 +12,7 @@ import threading
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnid.so")
+LIB_PATH = os.environ.get("NID_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnid.so")
 MAX_VARS = 16
 
 CONVERGED, AT_INFINITY_CODE, SINGULAR_ENDPOINT_CODE, FAILED_CODE = 0, 1, 2, 3

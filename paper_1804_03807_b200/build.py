@@ -32,6 +32,11 @@ if os.environ.get("NID_LU_FMA"):
     FLAGS = FLAGS + ["-DNID_LU_FMA"]
 if os.environ.get("NID_G10"):
     FLAGS = FLAGS + ["-DNID_G10=" + os.environ["NID_G10"]]
+# experiment variants: extra -D flags, objects in their own directory
+EXTRA = os.environ.get("NID_EXTRA_DEFS", "").split()
+if EXTRA:
+    FLAGS = FLAGS + EXTRA
+    OBJ = OBJ + "_" + "_".join(x.lstrip("-D").replace("=", "") for x in EXTRA)
 
 
 def _sources():
@@ -53,12 +58,14 @@ def _run(cmd):
     return r.stdout
 
 
-def build(jobs: int | None = None, verbose: bool = False, force: bool = False) -> str:
+def build(jobs: int | None = None, verbose: bool = False, force: bool = False, out: str | None = None,
+          sizes=None) -> str:
+    lib = out or LIB
     os.makedirs(OBJ, exist_ok=True)
     jobs = jobs or max(1, min(16, os.cpu_count() or 4))
     cmds = []
     objs = []
-    for n in SIZES:
+    for n in sizes or SIZES:
         o = os.path.join(OBJ, f"inst_{n}.o")
         objs.append(o)
         if force or _stale(o):
@@ -72,9 +79,9 @@ def build(jobs: int | None = None, verbose: bool = False, force: bool = False) -
             for out in ex.map(_run, cmds):
                 if verbose and out.strip():
                     print(out)
-    if cmds or force or not os.path.exists(LIB) or any(os.path.getmtime(x) > os.path.getmtime(LIB) for x in objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lnvrtc"])
-    return LIB
+    if cmds or force or not os.path.exists(lib) or any(os.path.getmtime(x) > os.path.getmtime(lib) for x in objs):
+        _run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-lnvrtc"])
+    return lib
 
 
 if __name__ == "__main__":
@@ -82,6 +89,7 @@ if __name__ == "__main__":
     ap.add_argument("--jobs", type=int, default=None)
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=None, help="library path (experiment variants)")
     a = ap.parse_args()
-    print(build(a.jobs, a.v, a.force))
+    print(build(a.jobs, a.v, a.force, a.out))
     sys.exit(0)

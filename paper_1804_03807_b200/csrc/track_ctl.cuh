@@ -71,6 +71,22 @@ struct Lay {
   }
 };
 
+// zgetf2's multiplier and rank-1 update (unfused unless NID_LU_FMA)
+NID_D cd lu_mul(cd a, cd inv) {
+#ifdef NID_LU_FMA
+  return a * inv;
+#else
+  return cmul_nf(a, inv);
+#endif
+}
+NID_D cd lu_upd(cd a, cd l, cd p) {
+#ifdef NID_LU_FMA
+  return cfms(a, l, p);
+#else
+  return csub_nf(a, cmul_nf(l, p));
+#endif
+}
+
 // blocks per SM the register budget is sized for: as many as the shared
 // memory admits (228 KB per SM, 1 KB reserved per block), at most 3
 template <int N>
@@ -627,21 +643,13 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>()) 
 #pragma unroll 1
             for (int pos = k + 1; pos < N; ++pos) {
               const int r = (perm >> (4 * pos)) & 15;
-#ifdef NID_LU_FMA
-              const cd l = A<N>(augs, r, k) * inv;
-#else
-              const cd l = cmul_nf(A<N>(augs, r, k), inv);
-#endif
+              const cd l = lu_mul(A<N>(augs, r, k), inv);
 #pragma unroll
               for (int m = 0; m < MC; ++m) {
                 const int j = k + 1 + q + m * G;
                 if (j <= N) {
                   cd& a = A<N>(augs, r, j);
-#ifdef NID_LU_FMA
-                  a = cfms(a, l, prow[m]);
-#else
-                  a = csub_nf(a, cmul_nf(l, prow[m]));
-#endif
+                  a = lu_upd(a, l, prow[m]);
                 }
               }
             }

@@ -250,21 +250,61 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
   }
 }
 
+// Terms k, k+1, ... of a row while their factor count is K (the host keeps
+// rows in table order; equal-count runs are the common case, e.g. every row
+// of the cyclic systems): one dispatch per run.  Returns the next term.
+template <int N, int K, bool ML>
+NID_D int fterm_run(const HomDev& H, int k, int k1, uint4 f, const cd* xs, const double* axs, bool ws, cd alpha,
+                    double t, const cd* prm, cd* row, cd& hv, double& sS, double& sT) {
+#pragma unroll 1
+  while (true) {
+    cd ct = ldg_c(H.ct + k);
+    if (H.pslot != nullptr) {
+      const int sl = __ldg(H.pslot + k);
+      if (sl >= 0) ct = prm[sl];
+    }
+    const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
+    double m;
+    fterm<N, K, ML>(H, k, f, xs, axs, ws, c, row, hv, m);
+    if (ws) {
+      if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
+      sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), m));
+    }
+    if (++k >= k1) break;
+    f = __ldg(H.fac + k);
+    if (f.z != (unsigned)K) break;
+  }
+  return k;
+}
+
 template <int N, bool ML>
-NID_D void fterm_dispatch(const HomDev& H, int k, const uint4 f, const cd* xs, const double* axs, bool ws, cd c,
-                          cd* row, cd& hv, double& m) {
+NID_D int fterm_dispatch(const HomDev& H, int k, int k1, const cd* xs, const double* axs, bool ws, cd alpha, double t,
+                         const cd* prm, cd* row, cd& hv, double& sS, double& sT) {
+  const uint4 f = __ldg(H.fac + k);
   switch (f.z) {
 #define NID_FT(KK) \
   case KK:         \
-    if (KK <= N) fterm<N, (KK <= N ? KK : 1), ML>(H, k, f, xs, axs, ws, c, row, hv, m); \
+    if (KK <= N) return fterm_run<N, (KK <= N ? KK : 1), ML>(H, k, k1, f, xs, axs, ws, alpha, t, prm, row, hv, sS, sT); \
     break;
     NID_FT(1) NID_FT(2) NID_FT(3) NID_FT(4) NID_FT(5) NID_FT(6) NID_FT(7) NID_FT(8)
     NID_FT(9) NID_FT(10) NID_FT(11) NID_FT(12) NID_FT(13) NID_FT(14) NID_FT(15) NID_FT(16)
 #undef NID_FT
-    default:  // constant term
-      hv = cfma(c, cd{1.0, 0.0}, hv);
-      m = 1.0;
+    default:
+      break;
   }
+  // constant term
+  cd ct = ldg_c(H.ct + k);
+  if (H.pslot != nullptr) {
+    const int sl = __ldg(H.pslot + k);
+    if (sl >= 0) ct = prm[sl];
+  }
+  const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
+  hv = cfma(c, cd{1.0, 0.0}, hv);
+  if (ws) {
+    if (!H.td) sS = __dadd_rn(sS, __ldg(H.acs + k));
+    sT = __dadd_rn(sT, __ldg(H.act + k));
+  }
+  return k + 1;
 }
 
 // Rows of warp group g into the slot's augmented matrix (as eval_rows).
@@ -291,23 +331,11 @@ NID_D void eval_rows_fac(const HomDev& H, int g, const cd* xs, double t, const c
     const int k0 = __ldg(H.row_off + i), k1 = __ldg(H.row_off + i + 1);
     double sS = 0.0, sT = 0.0;
 #pragma unroll 1
-    for (int k = k0; k < k1; ++k) {
-      const uint4 f = __ldg(H.fac + k);
-      cd ct = ldg_c(H.ct + k);
-      if (H.pslot != nullptr) {
-        const int sl = __ldg(H.pslot + k);
-        if (sl >= 0) ct = prm[sl];
-      }
-      const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
-      double m;
+    for (int k = k0; k < k1;) {
       if (H.multilinear) {
-        fterm_dispatch<N, true>(H, k, f, xs, axw, ws, c, row, hv, m);
+        k = fterm_dispatch<N, true>(H, k, k1, xs, axw, ws, alpha, t, prm, row, hv, sS, sT);
       } else {
-        fterm_dispatch<N, false>(H, k, f, xs, axw, ws, c, row, hv, m);
-      }
-      if (ws) {
-        if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
-        sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), m));
+        k = fterm_dispatch<N, false>(H, k, k1, xs, axw, ws, alpha, t, prm, row, hv, sS, sT);
       }
     }
     if (H.td) {  // G_i = x_i^{d_i} - 1 in closed form
