@@ -28,8 +28,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 SIZES = list(range(1, 17))
 if os.environ.get("NID_PHASE_TIMERS"):
     FLAGS = FLAGS + ["-DNID_PHASE_TIMERS"]
-if os.environ.get("NID_LU_FMA"):
-    FLAGS = FLAGS + ["-DNID_LU_FMA"]
+if os.environ.get("NID_LU_UNFUSED"):
+    FLAGS = FLAGS + ["-DNID_LU_UNFUSED"]
 if os.environ.get("NID_G10"):
     FLAGS = FLAGS + ["-DNID_G10=" + os.environ["NID_G10"]]
 # experiment variants: extra -D flags, objects in their own directory

@@ -71,19 +71,20 @@ struct Lay {
   }
 };
 
-// zgetf2's multiplier and rank-1 update (unfused unless NID_LU_FMA)
+// zgetf2's multiplier and rank-1 update, fused (NID_LU_UNFUSED: zgetf2's
+// separately rounded products, as the parity-hook kernels use)
 NID_D cd lu_mul(cd a, cd inv) {
-#ifdef NID_LU_FMA
-  return a * inv;
-#else
+#ifdef NID_LU_UNFUSED
   return cmul_nf(a, inv);
+#else
+  return a * inv;
 #endif
 }
 NID_D cd lu_upd(cd a, cd l, cd p) {
-#ifdef NID_LU_FMA
-  return cfms(a, l, p);
-#else
+#ifdef NID_LU_UNFUSED
   return csub_nf(a, cmul_nf(l, p));
+#else
+  return cfms(a, l, p);
 #endif
 }
 
@@ -676,8 +677,8 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>()) 
         const int r = (pm >> (4 * k)) & 15;
         cd s = A<N>(augc, r, N);
 #pragma unroll
-        for (int j = k + 1; j < N; ++j) s = csub_nf(s, cmul_nf(A<N>(augc, r, j), dx[j]));
-        dx[k] = cmul_nf(s, A<N>(augc, r, k));
+        for (int j = k + 1; j < N; ++j) s = lu_upd(s, A<N>(augc, r, j), dx[j]);
+        dx[k] = lu_mul(s, A<N>(augc, r, k));
         fin = fin && cfinite(dx[k]);
       }
       if (!C_IS(I_BAD) && fin) {
