@@ -204,6 +204,14 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
   cd P[K];
   uint4 fe = make_uint4(0u, 0u, 0u, 0u);
   if (!ML) fe = __ldg(H.fex + k);
+  // multilinear: the term's variables are distinct, so every Jacobian entry
+  // it touches is read up front (overlapping the prefix chain) and written
+  // once at the end -- no load-after-store chain through shared memory
+  cd Jv[ML ? K : 1];
+  if (ML) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) Jv[j] = row[(((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15) * SLOTS];
+  }
   cd p = cd{1.0, 0.0};
   m = 1.0;
 #pragma unroll
@@ -234,7 +242,7 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
     const cd x = xs[v * SLOTS];
     cd* const J = row + v * SLOTS;
     if (ML) {
-      *J = cfma(P[j], s, *J);
+      Jv[j] = cfma(P[j], s, Jv[j]);
       s = s * x;
     } else {
       const int a = ((j < 4 ? fe.x : (j < 8 ? fe.y : (j < 12 ? fe.z : fe.w))) >> (8 * (j & 3))) & 255;
@@ -247,6 +255,10 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
         s = s * (q * x);
       }
     }
+  }
+  if (ML) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) row[(((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15) * SLOTS] = Jv[j];
   }
 }
 
