@@ -267,6 +267,10 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
       fac[k] = make_uint4((unsigned)vl, (unsigned)(vl >> 32), (unsigned)nf, 0u);
       fex[k] = make_uint4(ex[0], ex[1], ex[2], ex[3]);
     }
+    // w: end of the run of equal factor counts starting at k (within its row)
+    for (int i = 0; i < n; ++i)
+      for (int k = off[i + 1] - 1; k >= off[i]; --k)
+        fac[k].w = (k + 1 < off[i + 1] && fac[k + 1].z == fac[k].z) ? fac[k + 1].w : (unsigned)(k + 1);
     e = cudaMemcpy(h->fac, fac.data(), T * sizeof(uint4), cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(h->fex, fex.data(), T * sizeof(uint4), cudaMemcpyHostToDevice);
   }

@@ -268,8 +268,11 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
 template <int N, int K, bool ML>
 NID_D int fterm_run(const HomDev& H, int k, int k1, uint4 f, const cd* xs, const double* axs, bool ws, cd alpha,
                     double t, const cd* prm, cd* row, cd& hv, double& sS, double& sT) {
+  const int kend = (int)f.w;  // the run's end, precomputed on the host
 #pragma unroll 1
-  while (true) {
+  for (;;) {
+    // the next term's factor list is fetched while this term computes
+    const uint4 fn = k + 1 < kend ? __ldg(H.fac + k + 1) : f;
     cd ct = ldg_c(H.ct + k);
     if (H.pslot != nullptr) {
       const int sl = __ldg(H.pslot + k);
@@ -282,9 +285,8 @@ NID_D int fterm_run(const HomDev& H, int k, int k1, uint4 f, const cd* xs, const
       if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
       sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), m));
     }
-    if (++k >= k1) break;
-    f = __ldg(H.fac + k);
-    if (f.z != (unsigned)K) break;
+    if (++k >= kend) break;
+    f = fn;
   }
   return k;
 }
