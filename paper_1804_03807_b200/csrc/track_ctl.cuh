@@ -640,11 +640,16 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>()) 
             const int j = k + 1 + q + m * G;
             if (j <= N) prow[m] = A<N>(augs, r0, j);
           }
-          if (solving) {
+          if (solving && k + 1 < N) {
+            // column k is not written in step k: the next row's multiplier
+            // source is loaded before this row's stores
+            int r = (perm >> (4 * (k + 1))) & 15;
+            cd ark = A<N>(augs, r, k);
 #pragma unroll 1
             for (int pos = k + 1; pos < N; ++pos) {
-              const int r = (perm >> (4 * pos)) & 15;
-              const cd l = lu_mul(A<N>(augs, r, k), inv);
+              const int rn = pos + 1 < N ? (int)((perm >> (4 * (pos + 1))) & 15) : r;
+              const cd arkn = A<N>(augs, rn, k);
+              const cd l = lu_mul(ark, inv);
 #pragma unroll
               for (int m = 0; m < MC; ++m) {
                 const int j = k + 1 + q + m * G;
@@ -653,6 +658,8 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>()) 
                   a = lu_upd(a, l, prow[m]);
                 }
               }
+              r = rn;
+              ark = arkn;
             }
           }
           __syncwarp();

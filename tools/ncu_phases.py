@@ -48,7 +48,7 @@ def main(csvp, ctl_src="paper_1804_03807_b200/csrc/track_ctl.cuh"):
             return PHASE_FILES[f]
         return None
 
-    rows = []
+    by_addr = {}
     hdr = None
     f = None
     cur = None
@@ -68,14 +68,28 @@ def main(csvp, ctl_src="paper_1804_03807_b200/csrc/track_ctl.cuh"):
             continue
         if hdr is None or not r[2].startswith("0x"):
             continue
-        rows.append((int(r[2], 16), cur, r))
-    rows.sort()
+        e = by_addr.setdefault(int(r[2], 16), [[], r])
+        e[0].append(cur)
     col = {h: i for i, h in enumerate(hdr)}
     stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
     agg = defaultdict(lambda: defaultdict(float))
     last = "control"
-    for addr, (fl, line), r in rows:
-        ph = phase_of(fl, line)
+    for addr in sorted(by_addr):
+        lines, r = by_addr[addr]
+        # an inlined instruction is listed under every line of its call chain:
+        # the kernel body's line decides, then the evaluator, then control
+        ph = None
+        for fl, line in lines:
+            if fl == "track_ctl.cuh" and ctl_fn_end and line >= ctl_fn_end:
+                ph = phase_of(fl, line)
+        if ph is None:
+            for fl, line in lines:
+                if fl in PHASE_FILES:
+                    ph = PHASE_FILES[fl]
+        if ph is None:
+            for fl, line in lines:
+                if fl == "track_ctl.cuh":
+                    ph = "control"
         if ph is None:
             ph = last
         else:
