@@ -214,10 +214,12 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
   }
   cd p = cd{1.0, 0.0};
   m = 1.0;
+  cd Xr[ML ? K : 1];  // multilinear: x kept for the suffix pass (no re-read)
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const int v = ((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15;
     const cd x = xs[v * SLOTS];
+    if (ML) Xr[j] = x;
     P[j] = p;
     if (ML) {
       p = p * x;
@@ -239,7 +241,7 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
 #pragma unroll
   for (int j = K - 1; j >= 0; --j) {
     const int v = ((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15;
-    const cd x = xs[v * SLOTS];
+    const cd x = ML ? Xr[j] : xs[v * SLOTS];
     cd* const J = row + v * SLOTS;
     if (ML) {
       Jv[j] = cfma(P[j], s, Jv[j]);
