@@ -129,7 +129,8 @@ int nid_svd_batch(int m, int n, int P, const double* A, double* sv);
  * system of the homotopy, with start path indices [first_index, first_index+P)
  * (mixed radix over `degrees`, last variable fastest).  Results go to host
  * buffers in `out`.  `device_io` != 0 means every pointer (starts, params,
- * out arrays) is a device pointer and nothing is copied.
+ * out arrays) is a device pointer and nothing is copied; the complex arrays
+ * (starts, params, x_end) must then be 16-byte aligned.
  */
 int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
                     long long first_index, const int32_t* degrees, const double* params,

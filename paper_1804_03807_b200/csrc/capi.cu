@@ -392,6 +392,9 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
   int* d_steps;
   double *d_tr, *d_res, *d_cond;
   if (device_io) {
+    // complex arrays are read/written as 128-bit words
+    if (((uintptr_t)starts | (uintptr_t)params | (uintptr_t)out->x_end) & 15)
+      FAIL("device_io: starts, params and x_end must be 16-byte aligned");
     d_starts = (const cd*)starts;
     d_params = (const cd*)params;
     d_x = (cd*)out->x_end;

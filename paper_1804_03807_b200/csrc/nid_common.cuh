@@ -23,7 +23,8 @@ typedef unsigned long long uint64_t;
 #define NID_HD __host__ __device__ __forceinline__
 #define NID_D __device__ __forceinline__
 
-struct cd {
+// 16-byte aligned so a complex loads/stores as one 128-bit access
+struct __align__(16) cd {
   double re, im;
 };
 
