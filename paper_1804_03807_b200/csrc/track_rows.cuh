@@ -199,34 +199,45 @@ NID_D void eval_rows(const HomDev& H, int g, const cd (&x)[N], double t, const c
 template <int N, int K, bool ML>
 NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const double* axs, bool ws, cd c, cd* row,
                  cd& hv, double& m) {
-  // only the prefix products stay live between the passes: indices,
-  // exponents and x are re-read (shared memory / the term's words)
+  // A term's variables are distinct, so every Jacobian entry it touches is
+  // read up front (overlapping the prefix chain) and written once at the
+  // end -- no load-after-store chain through shared memory.  x (and for
+  // exponents > 1 the powers) stay in registers between the two passes.
+  // Wide non-multilinear terms (K > 6) keep only the prefix products live.
+  constexpr bool BATCH = ML || K <= 6;
   cd P[K];
+  cd Xr[BATCH ? K : 1];
+  cd Qr[(!ML && BATCH) ? K : 1];
+  cd Jv[BATCH ? K : 1];
   uint4 fe = make_uint4(0u, 0u, 0u, 0u);
   if (!ML) fe = __ldg(H.fex + k);
-  // multilinear: the term's variables are distinct, so every Jacobian entry
-  // it touches is read up front (overlapping the prefix chain) and written
-  // once at the end -- no load-after-store chain through shared memory
-  cd Jv[ML ? K : 1];
-  if (ML) {
+  if (BATCH) {
 #pragma unroll
     for (int j = 0; j < K; ++j) Jv[j] = row[(((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15) * SLOTS];
   }
   cd p = cd{1.0, 0.0};
   m = 1.0;
-  cd Xr[ML ? K : 1];  // multilinear: x kept for the suffix pass (no re-read)
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const int v = ((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15;
     const cd x = xs[v * SLOTS];
-    if (ML) Xr[j] = x;
     P[j] = p;
     if (ML) {
+      Xr[j] = x;
       p = p * x;
       if (ws) m = __dmul_rn(m, axs[v * SLOTS]);
     } else {
       const int a = ((j < 4 ? fe.x : (j < 8 ? fe.y : (j < 12 ? fe.z : fe.w))) >> (8 * (j & 3))) & 255;
-      p = p * (a == 1 ? x : upow(x, a));
+      if (BATCH) {
+        // x^a = x^(a-1) * x, the same products as upow(x, a)
+        const cd q = a == 1 ? cd{1.0, 0.0} : upow(x, a - 1);
+        const cd xa = a == 1 ? x : q * x;
+        Qr[j] = q;
+        Xr[j] = xa;
+        p = p * xa;
+      } else {
+        p = p * (a == 1 ? x : upow(x, a));
+      }
       if (ws) {
         const double ax = axs[v * SLOTS];
         double pv = ax;
@@ -240,13 +251,21 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
   cd s = c;
 #pragma unroll
   for (int j = K - 1; j >= 0; --j) {
-    const int v = ((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15;
-    const cd x = ML ? Xr[j] : xs[v * SLOTS];
-    cd* const J = row + v * SLOTS;
     if (ML) {
       Jv[j] = cfma(P[j], s, Jv[j]);
-      s = s * x;
+      s = s * Xr[j];
+    } else if (BATCH) {
+      const int a = ((j < 4 ? fe.x : (j < 8 ? fe.y : (j < 12 ? fe.z : fe.w))) >> (8 * (j & 3))) & 255;
+      if (a == 1) {
+        Jv[j] = cfma(P[j], s, Jv[j]);
+      } else {
+        Jv[j] = cfma(P[j] * ((double)a * Qr[j]), s, Jv[j]);
+      }
+      s = s * Xr[j];
     } else {
+      const int v = ((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15;
+      const cd x = xs[v * SLOTS];
+      cd* const J = row + v * SLOTS;
       const int a = ((j < 4 ? fe.x : (j < 8 ? fe.y : (j < 12 ? fe.z : fe.w))) >> (8 * (j & 3))) & 255;
       if (a == 1) {
         *J = cfma(P[j], s, *J);
@@ -258,7 +277,7 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
       }
     }
   }
-  if (ML) {
+  if (BATCH) {
 #pragma unroll
     for (int j = 0; j < K; ++j) row[(((j < 8 ? f.x : f.y) >> (4 * (j & 7))) & 15) * SLOTS] = Jv[j];
   }
