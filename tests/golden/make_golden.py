@@ -144,6 +144,18 @@ def gen_track_c5():
     save("track_c5_sample", **track_problem(p5, idx))
 
 
+def gen_track_c5_large():
+    """16,384 seeded uniform C5 paths: pins the finite count and per-path
+    statuses at a sample size where the finite fraction (~0.9 %) is measurable.
+    Stored compactly: statuses and steps for all, endpoints of finite paths."""
+    p5 = configs.c5()
+    idx = np.sort(np.random.default_rng(6).choice(p5.paths, size=16384, replace=False))
+    d = track_problem(p5, idx)
+    fin = np.isin(d["status"], (0, 2))
+    save("track_c5_large", index=d["index"], status=d["status"], steps=d["steps"].astype(np.int16),
+         fin_x=d["x"][fin], fin_regular=d["regular"][fin])
+
+
 def gen_track_c3():
     pd = configs.c3()
     p = configs.c3_top(pd)
@@ -289,7 +301,7 @@ def gen_dedup():
     save("dedup_golden", x=pts, res=np.array(res), kept=np.array(idx))
 
 
-GENS = {"eval": gen_eval, "linalg": gen_linalg, "track_small": gen_track_small, "track_c5": gen_track_c5,
+GENS = {"eval": gen_eval, "linalg": gen_linalg, "track_small": gen_track_small, "track_c5": gen_track_c5, "track_c5_large": gen_track_c5_large,
         "track_c3": gen_track_c3, "pipeline_c3m": gen_pipeline_c3m, "membership_c3m": gen_membership_c3m,
         "refine": gen_refine, "dd": gen_dd, "dedup": gen_dedup}
 
