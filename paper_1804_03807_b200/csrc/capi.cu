@@ -4,6 +4,7 @@
 #include <nvrtc.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -46,6 +47,7 @@ struct NidHomotopy {
   cd *cs, *ct;
   double *acs, *act;
   int8_t* pslot;
+  PTab* ptab = nullptr;  // host copy of the parameter-bank table (null: table too large / per-path params)
   cudaLibrary_t jit_lib = nullptr;  // NVRTC-specialised tracker (nid_homotopy_jit)
   cudaKernel_t jit_kernel = nullptr;
   HomDev dev() const {
@@ -106,6 +108,9 @@ typedef int (*EvalFn)(const EvalArgs&, int, cudaStream_t);
 typedef int (*NewtonFn)(const NewtonArgs&, int, cudaStream_t);
 typedef int (*RegsFn)();
 static const TrackFn k_track[17] = NID_TABLE(launch_track_);
+typedef int (*TrackPTFn)(const TrackArgsPT&, int, cudaStream_t);
+static const TrackPTFn k_track_pt[17] = NID_TABLE(launch_track_pt_);
+static const RegsFn k_pt_regs[17] = NID_TABLE(track_pt_regs_);
 static const EndpointFn k_endpoint[17] = NID_TABLE(launch_endpoint_);
 static const RefineFn k_refine[17] = NID_TABLE(launch_refine_);
 static const DDRefineFn k_ddrefine[17] = NID_TABLE(launch_ddrefine_);
@@ -271,6 +276,48 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
     for (int i = 0; i < n; ++i)
       for (int k = off[i + 1] - 1; k >= off[i]; --k)
         fac[k].w = (k + 1 < off[i + 1] && fac[k + 1].z == fac[k].z) ? fac[k + 1].w : (unsigned)(k + 1);
+    // the parameter-bank table (csrc/track_ptab.cuh) when the system fits it
+    if (!d->param_slot && T <= PT_MAXT) {
+      PTab* pt = new PTab();
+      memset(pt, 0, sizeof(PTab));
+      int nr = 0, nf = 0;
+      bool fits = true;
+      for (int i = 0; i < n && fits; ++i) {
+        pt->row_run[i] = (unsigned short)nr;
+        for (int k = off[i]; k < off[i + 1] && fits;) {
+          const int K = (int)fac[k].z;
+          int k1 = k;
+          while (k1 < off[i + 1] && (int)fac[k1].z == K && k1 - k < 255) ++k1;
+          if (nr >= PT_MAXR || nf + (k1 - k) * K > PT_MAXF) {
+            fits = false;
+            break;
+          }
+          pt->run_k0[nr] = (unsigned short)k;
+          pt->run_f0[nr] = (unsigned short)nf;
+          pt->run_K[nr] = (unsigned char)K;
+          pt->run_n[nr] = (unsigned char)(k1 - k);
+          ++nr;
+          for (int kk = k; kk < k1; ++kk)
+            for (int v = 0; v < n; ++v) {
+              const int a = d->expo[kk * NID_MAX_VARS + v];
+              if (!a) continue;
+              pt->foff[nf] = (unsigned)(v * rows::SLOTS * sizeof(cd));
+              pt->fexp[nf] = (unsigned char)a;
+              ++nf;
+            }
+          k = k1;
+        }
+      }
+      pt->row_run[n] = (unsigned short)nr;
+      for (int k = 0; k < T && fits; ++k) {
+        pt->ct[k] = cd{d->coef_target[2 * k], d->coef_target[2 * k + 1]};
+        pt->cs[k] = cd{d->coef_start[2 * k], d->coef_start[2 * k + 1]};
+        pt->act[k] = act[k];
+        pt->acs[k] = acs[k];
+      }
+      if (fits) h->ptab = pt;
+      else delete pt;
+    }
     e = cudaMemcpy(h->fac, fac.data(), T * sizeof(uint4), cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(h->fex, fex.data(), T * sizeof(uint4), cudaMemcpyHostToDevice);
   }
@@ -341,6 +388,7 @@ int nid_homotopy_destroy(NidHomotopy* h) {
   if (h->jit_lib) cudaLibraryUnload(h->jit_lib);
   cudaFree(h->row_off);
   cudaFree(h->expo);
+  delete h->ptab;
   cudaFree(h->fac);
   cudaFree(h->fex);
   cudaFree(h->cs);
@@ -491,6 +539,12 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
     if (need < blocks) blocks = need;
     void* args[] = {(void*)&a};
     CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, (size_t)smem, s));
+  } else if (h->ptab && !getenv("NID_NO_PTAB")) {
+    TrackArgsPT* pa = new TrackArgsPT;  // ~22 KB: off the stack
+    pa->a = a;
+    pa->t = *h->ptab;
+    k_track_pt[n](*pa, max_blocks, s);
+    delete pa;
   } else {
     k_track[n](a, max_blocks, s);
   }

@@ -39,6 +39,21 @@ int CAT(launch_track_, NID_N)(const TrackArgs& a, int max_blocks, cudaStream_t s
   return blocks;
 }
 
+// the same tracker with the term table in the launch's parameter bank
+int CAT(launch_track_pt_, NID_N)(const TrackArgsPT& a, int max_blocks, cudaStream_t s) {
+  const void* fn = (const void*)track_pt_kernel<NID_N>;
+  const int threads = 32 * rows::groups<NID_N>();
+  const int smem = (int)ctl::Lay<NID_N>::bytes();
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int blocks = blocks_for(fn, threads, smem);
+  long long need = (a.a.P + rows::SLOTS - 1) / rows::SLOTS;
+  if (need < blocks) blocks = (int)need;
+  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
+  if (blocks < 1) blocks = 1;
+  track_pt_kernel<NID_N><<<blocks, threads, smem, s>>>(a);
+  return blocks;
+}
+
 int CAT(launch_endpoint_, NID_N)(const EndpointArgs& a, int blocks, cudaStream_t s) {
   endpoint_kernel<NID_N><<<blocks, 128, 0, s>>>(a);
   return blocks;
@@ -67,6 +82,12 @@ int CAT(launch_newton_, NID_N)(const NewtonArgs& a, int blocks, cudaStream_t s) 
 int CAT(track_regs_, NID_N)() {
   cudaFuncAttributes at;
   if (cudaFuncGetAttributes(&at, (const void*)track_ctl_kernel<NID_N>) != cudaSuccess) return -1;
+  return at.numRegs;
+}
+
+int CAT(track_pt_regs_, NID_N)() {
+  cudaFuncAttributes at;
+  if (cudaFuncGetAttributes(&at, (const void*)track_pt_kernel<NID_N>) != cudaSuccess) return -1;
   return at.numRegs;
 }
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 struct TrackArgs;
+struct TrackArgsPT;
 struct EndpointArgs;
 struct RefineArgs;
 struct DDRefineArgs;
@@ -12,6 +13,8 @@ struct NewtonArgs;
 namespace nid {
 #define NID_DECL(n)                                                        \
   int launch_track_##n(const TrackArgs&, int, cudaStream_t);               \
+  int launch_track_pt_##n(const TrackArgsPT&, int, cudaStream_t);          \
+  int track_pt_regs_##n();                                                  \
   int launch_endpoint_##n(const EndpointArgs&, int, cudaStream_t);         \
   int launch_refine_##n(const RefineArgs&, int, cudaStream_t);             \
   int launch_ddrefine_##n(const DDRefineArgs&, int, cudaStream_t);         \

@@ -27,11 +27,20 @@
 // (izamax on |Re|+|Im| in row-swap order, unfused updates) with the zgelsd
 // min-norm fallback (solved by the controller lane on a global scratch copy).
 #pragma once
+#include "track_ptab.cuh"
 #include "track_rows.cuh"
 
 namespace ctl {
 
 using rows::A;
+template <class T>
+struct is_ptab {
+  static constexpr bool value = false;
+};
+template <>
+struct is_ptab<PTab> {
+  static constexpr bool value = true;
+};
 using rows::SLOTS;
 
 // slot state, struct of arrays [field][slot]
@@ -482,8 +491,12 @@ struct TableEval {
 #define NID_TP(i)
 #endif
 
-template <int N, class Eval = TableEval<N>>
-__global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>()) track_ctl_kernel(const __grid_constant__ TrackArgs Ar) {
+// The kernel body, shared by the table-driven kernel (track_ctl_kernel: term
+// table in global memory, read through L1) and the parameter-table kernel
+// (track_pt_kernel: csrc/track_ptab.cuh, the table in the launch's constant
+// bank).  Tab = void selects Eval; Tab = PTab selects PTEval.
+template <int N, class Eval, class Tab>
+__device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) {
   using namespace ctl;
   using L = Lay<N>;
   constexpr int G = L::G;
@@ -527,13 +540,17 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>()) 
     if (!__syncthreads_or(W_IS(I_ACT) != A_IDLE)) break;
     NID_TP(1);  // barrier before the evaluation
     if (W_IS(I_ACT) == A_EVAL) {
-      cd x[N];
+      const bool want = (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
+      if constexpr (ctl::is_ptab<Tab>::value) {
+        PTEval<N>::rows(Ar.H, *tab, g, W_DS(D_TE), aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);
+      } else {
+        cd x[N];
 #pragma unroll
-      for (int v = 0; v < N; ++v) x[v] = cb[(L::XE + v) * S + lane];
-      const long long pr = lb[S + lane];
-      const cd* prm = pr >= 0 ? Ar.params + pr : nullptr;
-      Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0,
-                 cb + L::XE * S + lane, db + L::AXW * S + lane);
+        for (int v = 0; v < N; ++v) x[v] = cb[(L::XE + v) * S + lane];
+        const long long pr = lb[S + lane];
+        const cd* prm = pr >= 0 ? Ar.params + pr : nullptr;
+        Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);
+      }
     }
     NID_TP(2);  // evaluation
     __syncthreads();
@@ -738,4 +755,16 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>()) 
     atomicAdd(Ar.counters + 2, n_scale);
     atomicAdd(Ar.counters + 3, n_fb);
   }
+}
+
+template <int N, class Eval = TableEval<N>>
+__global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>())
+    track_ctl_kernel(const __grid_constant__ TrackArgs Ar) {
+  track_body<N, Eval, void>(Ar, nullptr);
+}
+
+template <int N>
+__global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>())
+    track_pt_kernel(const __grid_constant__ TrackArgsPT A) {
+  track_body<N, TableEval<N>, PTab>(A.a, &A.t);
 }
