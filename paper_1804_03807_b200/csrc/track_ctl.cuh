@@ -97,6 +97,90 @@ NID_D cd lu_upd(cd a, cd l, cd p) {
 #endif
 }
 
+// One elimination step k of the warp-local column-split LU (track_body):
+// pivot search over the slot's G lanes, implicit row swap, multipliers and
+// the rank-1 update of the remaining rows.  MCK = ceil((N-k)/G), the most
+// columns (and candidate pivot rows) a lane owns at this k: the k loop is
+// split into runs of equal MCK so no predicated-off column update is issued.
+template <int N, int G, int CPW, int MCK>
+NID_D void lu_step(cd* augs, int k, int q, bool solving, unsigned long long& perm, bool& bad) {
+  // izamax over the slot's G lanes as one 64-bit max: a candidate's key
+  // |Re|+|Im| (> 0, so its bit pattern orders like the value) with the low 4
+  // mantissa bits replaced by 15 - position, so equal keys resolve to the
+  // first position as izamax does (keys within 16 ulps count as equal).
+  // Zero / NaN keys encode 0: no usable pivot.
+  unsigned long long best = 0ull;
+#pragma unroll
+  for (int m = 0; m < MCK; ++m) {
+    const int pos = k + q + m * G;
+    if (pos < N) {
+      const int r = (perm >> (4 * pos)) & 15;
+      const double key = cabs1(rows::A<N>(augs, r, k));
+      const unsigned long long u =
+          key > 0.0 ? ((unsigned long long)__double_as_longlong(key) & ~15ull) | (unsigned long long)(15 - pos) : 0ull;
+      best = u > best ? u : best;
+    }
+  }
+#pragma unroll
+  for (int m = CPW; m < 32; m <<= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, m);
+    best = o > best ? o : best;
+  }
+  if (best == 0ull) bad = true;
+  const int pk = best == 0ull ? k : 15 - (int)(best & 15ull);
+  const unsigned long long rk = (perm >> (4 * k)) & 15, rp = (perm >> (4 * pk)) & 15;
+  perm &= ~((15ull << (4 * k)) | (15ull << (4 * pk)));
+  perm |= (rp << (4 * k)) | (rk << (4 * pk));
+  const int r0 = (int)rp;
+  const cd inv = crecip_fast(rows::A<N>(augs, r0, k));
+  // column slots past the last column read column N (valid, unused): the
+  // arrays are written unconditionally and stay in registers
+  cd prow[MCK];
+#pragma unroll
+  for (int m = 0; m < MCK; ++m) prow[m] = rows::A<N>(augs, r0, min(k + 1 + q + m * G, N));
+  if (solving && k + 1 < N) {
+    // software-pipelined over rows: the next row's multiplier source and
+    // columns are loaded before this row's update and stores (distinct
+    // rows; column k is not written in step k), so the shared-memory load
+    // latency overlaps the FMAs
+    const bool lastok = k + 1 + q + (MCK - 1) * G <= N;  // only the last column slot can fall off the end
+    int r = (perm >> (4 * (k + 1))) & 15;
+    cd ark = rows::A<N>(augs, r, k);
+    cd av[MCK];
+#pragma unroll
+    for (int m = 0; m < MCK; ++m) av[m] = rows::A<N>(augs, r, min(k + 1 + q + m * G, N));
+#pragma unroll 1
+    for (int pos = k + 1; pos < N; ++pos) {
+      const int rn = pos + 1 < N ? (int)((perm >> (4 * (pos + 1))) & 15) : r;
+      const cd arkn = rows::A<N>(augs, rn, k);
+      cd avn[MCK];
+#pragma unroll
+      for (int m = 0; m < MCK; ++m) avn[m] = rows::A<N>(augs, rn, min(k + 1 + q + m * G, N));
+      const cd l = lu_mul(ark, inv);
+#pragma unroll
+      for (int m = 0; m < MCK; ++m)
+        if (m < MCK - 1 || lastok) rows::A<N>(augs, r, k + 1 + q + m * G) = lu_upd(av[m], l, prow[m]);
+      r = rn;
+      ark = arkn;
+#pragma unroll
+      for (int m = 0; m < MCK; ++m) av[m] = avn[m];
+    }
+  }
+  __syncwarp();
+  // the pivot's reciprocal replaces it (the back substitution multiplies)
+  if (solving && q == 0) rows::A<N>(augs, r0, k) = inv;
+}
+
+// the k range [k0, N) split into runs of equal ceil((N-k)/G)
+template <int N, int G, int CPW, int MCK>
+NID_D void lu_run(cd* augs, int q, bool solving, unsigned long long& perm, bool& bad) {
+  constexpr int kb = N - MCK * G > 0 ? N - MCK * G : 0;  // first k with ceil((N-k)/G) == MCK
+  constexpr int ke = N - (MCK - 1) * G;                   // one past the last
+#pragma unroll 1
+  for (int k = kb; k < ke; ++k) lu_step<N, G, CPW, MCK>(augs, k, q, solving, perm, bad);
+  if constexpr (MCK > 1) lu_run<N, G, CPW, MCK - 1>(augs, q, solving, perm, bad);
+}
+
 // blocks per SM the register budget is sized for: as many as the shared
 // memory admits (228 KB per SM, 1 KB reserved per block), at most 3
 template <int N>
@@ -281,9 +365,18 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
           continue;
         }
         if (HAS(F_COK)) {
-          double m = 0.0;
-          for (int v = 0; v < N; ++v) m = nanmax(m, cabs_fast(xes[v * S]));
-          if (m > q.infinity_threshold) {
+          // ||x||_inf > threshold, decided on squared moduli (no square roots);
+          // the exact moduli only within 1e-12 of the threshold
+          double m2 = 0.0;
+          for (int v = 0; v < N; ++v) m2 = nanmax(m2, cabs2(xes[v * S]));
+          const double th2 = q.infinity_threshold * q.infinity_threshold;
+          bool inf_x = m2 > th2 * (1.0 + 1e-12) || isnan(m2);
+          if (!inf_x && m2 >= th2 * (1.0 - 1e-12)) {
+            double m = 0.0;
+            for (int v = 0; v < N; ++v) m = nanmax(m, cabs_fast(xes[v * S]));
+            inf_x = m > q.infinity_threshold;
+          }
+          if (inf_x) {
             IS_(I_OUTST) = NID_AT_INFINITY;
             SETF(F_HASX, false);
             DS_(D_OUTT) = DS_(D_TTRY);
@@ -535,6 +628,18 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
   while (true) {
     NID_T0();
     if (is_ctl) control<N>(Ar, V, augc + N * S);
+    __syncwarp();
+    {
+      // |x_v| of the evaluation points of this warp's slots that need the
+      // noise scale, spread over all 32 lanes (slot g*CPW + lane % CPW,
+      // variables lane / CPW + j * G); the evaluator reads them after the
+      // barrier instead of every warp recomputing all N moduli
+      const int sl = g * CPW + lane % CPW;
+      if (ib[I_ACT * S + sl] == A_EVAL && (ib[I_FLAGS * S + sl] & (F_NEEDSCALE | F_FALLBACK))) {
+#pragma unroll
+        for (int v = lane / CPW; v < N; v += G) db[(L::AXW + v) * S + sl] = cabs_fast(cb[(L::XE + v) * S + sl]);
+      }
+    }
     NID_TP(0);  // control (top)
     // ------------------------------------------------------------ evaluation
     if (!__syncthreads_or(W_IS(I_ACT) != A_IDLE)) break;
@@ -618,71 +723,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
 #pragma unroll
         for (int i = 0; i < N; ++i) perm |= (unsigned long long)i << (4 * i);
         bool bad = false;
-#pragma unroll 1
-        for (int k = 0; k < N; ++k) {
-          double best = -1.0;
-          int bpos = N;
-#pragma unroll
-          for (int m = 0; m < (N + G - 1) / G; ++m) {
-            const int pos = k + q + m * G;
-            if (pos < N) {
-              const int r = (perm >> (4 * pos)) & 15;
-              const double key = cabs1(A<N>(augs, r, k));
-              if (key > best) {  // positions ascend with m: first max wins ties
-                best = key;
-                bpos = pos;
-              }
-            }
-          }
-#pragma unroll
-          for (int m = CPW; m < 32; m <<= 1) {  // first max of |Re|+|Im| in logical order
-            const double ok = __shfl_xor_sync(0xffffffffu, best, m);
-            const int op = __shfl_xor_sync(0xffffffffu, bpos, m);
-            if (op < N && (bpos >= N || ok > best || (ok == best && op < bpos))) {
-              best = ok;
-              bpos = op;
-            }
-          }
-          const int pk = bpos < N ? bpos : k;
-          if (!(best > 0.0)) bad = true;
-          const unsigned long long rk = (perm >> (4 * k)) & 15, rp = (perm >> (4 * pk)) & 15;
-          perm &= ~((15ull << (4 * k)) | (15ull << (4 * pk)));
-          perm |= (rp << (4 * k)) | (rk << (4 * pk));
-          const int r0 = (int)rp;
-          const cd inv = crecip_fast(A<N>(augs, r0, k));
-          constexpr int MC = (N + G - 1) / G;  // most columns a lane owns
-          cd prow[MC];
-#pragma unroll
-          for (int m = 0; m < MC; ++m) {
-            const int j = k + 1 + q + m * G;
-            if (j <= N) prow[m] = A<N>(augs, r0, j);
-          }
-          if (solving && k + 1 < N) {
-            // column k is not written in step k: the next row's multiplier
-            // source is loaded before this row's stores
-            int r = (perm >> (4 * (k + 1))) & 15;
-            cd ark = A<N>(augs, r, k);
-#pragma unroll 1
-            for (int pos = k + 1; pos < N; ++pos) {
-              const int rn = pos + 1 < N ? (int)((perm >> (4 * (pos + 1))) & 15) : r;
-              const cd arkn = A<N>(augs, rn, k);
-              const cd l = lu_mul(ark, inv);
-#pragma unroll
-              for (int m = 0; m < MC; ++m) {
-                const int j = k + 1 + q + m * G;
-                if (j <= N) {
-                  cd& a = A<N>(augs, r, j);
-                  a = lu_upd(a, l, prow[m]);
-                }
-              }
-              r = rn;
-              ark = arkn;
-            }
-          }
-          __syncwarp();
-          // the pivot's reciprocal replaces it (the back substitution multiplies)
-          if (solving && q == 0) A<N>(augs, r0, k) = inv;
-        }
+        lu_run<N, G, CPW, (N + G - 1) / G>(augs, q, solving, perm, bad);
         if (solving && q == 0) {
           lb[2 * S + ss] = (long long)perm;
           ib[I_BAD * S + ss] = bad ? 1 : 0;

@@ -57,7 +57,11 @@ template <int N, int K, bool ML>
 NID_D void run(const PTab& T, int r, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, cd* row,
                cd& hv, double& sS, double& sT) {
   const int k0 = T.run_k0[r], cnt = T.run_n[r], f0 = T.run_f0[r];
-#pragma unroll 1
+#ifndef NID_PT_UNROLL_K
+#define NID_PT_UNROLL_K 0
+#endif
+  constexpr int UNR = K <= NID_PT_UNROLL_K ? 2 : 1;
+#pragma unroll UNR
   for (int j = 0; j < cnt; ++j) {
     const int k = k0 + j, fb = f0 + j * K;
     const cd ct = T.ct[k];
@@ -173,10 +177,7 @@ struct PTEval {
     const cd alpha = (1.0 - t) * H.gamma;
     const bool ws = __any_sync(__activemask(), want_scale);
     const bool td = H.td != 0;
-    if (ws) {
-#pragma unroll
-      for (int v = 0; v < N; ++v) axw[v * S] = cabs_fast(xs[v * S]);
-    }
+    // axw: |x_v|, written by the tracker before the evaluation barrier
     double r2 = 0.0, mS = 0.0, mT = 0.0;
     // the warp's group index through a shuffle: the compiler then treats it
     // (and every table word addressed from it) as warp-uniform, so the table

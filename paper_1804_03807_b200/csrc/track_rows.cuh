@@ -351,10 +351,7 @@ NID_D void eval_rows_fac(const HomDev& H, int g, const cd* xs, double t, const c
   using L = Layout<N>;
   const cd alpha = (1.0 - t) * H.gamma;
   const bool ws = __any_sync(__activemask(), want_scale);
-  if (ws) {
-#pragma unroll
-    for (int v = 0; v < N; ++v) axw[v * SLOTS] = cabs_fast(xs[v * SLOTS]);
-  }
+  // axw: |x_v|, written by the tracker (track_body) before the evaluation barrier
   double r2 = 0.0, mS = 0.0, mT = 0.0;
 #pragma unroll 1
   for (int gi = H.goff[g]; gi < H.goff[g + 1]; ++gi) {

@@ -12,7 +12,7 @@ python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launches_${TAG}.log 2>&1
 python tools/probe_c5.py 200000 > gpurun_out/plain_probe_${TAG}.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:track_ctl -c 1 -o gpurun_out/prof_track_${TAG} \
+ncu --set full --clock-control none --import-source on -k regex:track_ -c 1 -o gpurun_out/prof_track_${TAG} \
   python tools/probe_c5.py 200000 > gpurun_out/ncu_full_${TAG}.log 2>&1
 tail -n 2 gpurun_out/bench_${TAG}.log gpurun_out/ref_arm_${TAG}.log gpurun_out/torchrun_${TAG}.log \
   gpurun_out/ncu_launches_${TAG}.log gpurun_out/ncu_full_${TAG}.log

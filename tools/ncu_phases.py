@@ -14,7 +14,7 @@ from collections import defaultdict
 
 # (file, first line, last line, phase) -- track_ctl.cuh line ranges are read
 # from markers in the source instead of hard-coding numbers
-PHASE_FILES = {"track_rows.cuh": "eval"}
+PHASE_FILES = {"track_rows.cuh": "eval", "track_ptab.cuh": "eval"}
 
 
 def ctl_ranges(path):
@@ -33,12 +33,19 @@ def main(csvp, ctl_src="paper_1804_03807_b200/csrc/track_ctl.cuh"):
              ("post_eval", marks["NID_TP(3)"], marks["NID_TP(4)"]), ("lu", marks["NID_TP(4)"], marks["NID_TP(5)"]),
              ("backsub", marks["NID_TP(5)"], marks["NID_TP(6)"]), ("tail", marks["NID_TP(6)"], 10 ** 9)]
     ctl_fn_end = None
+    lu_lo = lu_hi = None
     for i, l in enumerate(open(ctl_src), 1):
-        if "track_ctl_kernel(" in l and "__global__" in l:
+        if "void track_body(" in l:
             ctl_fn_end = i
+        if "NID_D void lu_step" in l and lu_lo is None:
+            lu_lo = i
+        if "// blocks per SM" in l:
+            lu_hi = i
 
     def phase_of(f, line):
         if f == "track_ctl.cuh":
+            if lu_lo and lu_lo <= line < lu_hi:
+                return "lu"
             if ctl_fn_end and line < ctl_fn_end:
                 return "control"
             for name, a, b in order:
@@ -80,7 +87,10 @@ def main(csvp, ctl_src="paper_1804_03807_b200/csrc/track_ctl.cuh"):
         # the kernel body's line decides, then the evaluator, then control
         ph = None
         for fl, line in lines:
-            if fl == "track_ctl.cuh" and ctl_fn_end and line >= ctl_fn_end:
+            if fl == "track_ctl.cuh" and lu_lo and lu_lo <= line < lu_hi:
+                ph = "lu"
+        for fl, line in lines:
+            if ph is None and fl == "track_ctl.cuh" and ctl_fn_end and line >= ctl_fn_end:
                 ph = phase_of(fl, line)
         if ph is None:
             for fl, line in lines:
