@@ -139,31 +139,24 @@ NID_D void lu_step(cd* augs, int k, int q, bool solving, unsigned long long& per
 #pragma unroll
   for (int m = 0; m < MCK; ++m) prow[m] = rows::A<N>(augs, r0, min(k + 1 + q + m * G, N));
   if (solving && k + 1 < N) {
-    // software-pipelined over rows: the next row's multiplier source and
-    // columns are loaded before this row's update and stores (distinct
-    // rows; column k is not written in step k), so the shared-memory load
-    // latency overlaps the FMAs
+    // column k is not written in step k: the next row's multiplier
+    // source is loaded before this row's stores
     const bool lastok = k + 1 + q + (MCK - 1) * G <= N;  // only the last column slot can fall off the end
     int r = (perm >> (4 * (k + 1))) & 15;
     cd ark = rows::A<N>(augs, r, k);
-    cd av[MCK];
-#pragma unroll
-    for (int m = 0; m < MCK; ++m) av[m] = rows::A<N>(augs, r, min(k + 1 + q + m * G, N));
 #pragma unroll 1
     for (int pos = k + 1; pos < N; ++pos) {
       const int rn = pos + 1 < N ? (int)((perm >> (4 * (pos + 1))) & 15) : r;
       const cd arkn = rows::A<N>(augs, rn, k);
-      cd avn[MCK];
-#pragma unroll
-      for (int m = 0; m < MCK; ++m) avn[m] = rows::A<N>(augs, rn, min(k + 1 + q + m * G, N));
       const cd l = lu_mul(ark, inv);
 #pragma unroll
       for (int m = 0; m < MCK; ++m)
-        if (m < MCK - 1 || lastok) rows::A<N>(augs, r, k + 1 + q + m * G) = lu_upd(av[m], l, prow[m]);
+        if (m < MCK - 1 || lastok) {
+          cd& a = rows::A<N>(augs, r, k + 1 + q + m * G);
+          a = lu_upd(a, l, prow[m]);
+        }
       r = rn;
       ark = arkn;
-#pragma unroll
-      for (int m = 0; m < MCK; ++m) av[m] = avn[m];
     }
   }
   __syncwarp();
