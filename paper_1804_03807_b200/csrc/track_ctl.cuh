@@ -201,6 +201,41 @@ struct SlotView {
 #define HAS(fl) ((IS_(I_FLAGS) & (fl)) != 0)
 #define SETF(fl, on) (IS_(I_FLAGS) = (on) ? (IS_(I_FLAGS) | (fl)) : (IS_(I_FLAGS) & ~(fl)))
 
+// the start point of path `path` into the slot's evaluation point: an
+// explicit start list, or a total-degree root generated from the path index
+// (mixed radix, last variable fastest).  Out of line: once per path, and the
+// 64-bit divisions would otherwise sit in the hot loop's instruction stream.
+#ifdef NID_CLAIM_INLINE
+#define NID_CLAIM_ATTR __forceinline__
+#else
+#define NID_CLAIM_ATTR __noinline__
+#endif
+template <int N>
+__device__ NID_CLAIM_ATTR void load_start(const TrackArgs& Ar, long long path, cd* xes) {
+  constexpr int S = SLOTS;
+  if (Ar.starts) {
+    for (int v = 0; v < N; ++v) xes[v * S] = Ar.starts[path * N + v];
+  } else {
+    long long rem = Ar.first_index + path;
+    if (rem < (1ll << 32)) {  // 32-bit digits (every config here)
+      unsigned r32 = (unsigned)rem;
+      for (int v = N - 1; v >= 0; --v) {
+        const unsigned d = (unsigned)Ar.deg[v];
+        const unsigned k = r32 % d;
+        r32 /= d;
+        xes[v * S] = Ar.roots[Ar.root_off[v] + (int)k];
+      }
+    } else {
+      for (int v = N - 1; v >= 0; --v) {
+        const int d = Ar.deg[v];
+        const long long k = rem % d;
+        rem /= d;
+        xes[v * S] = Ar.roots[Ar.root_off[v] + (int)k];
+      }
+    }
+  }
+}
+
 // The controller: runs slot transitions until the slot needs an evaluation
 // or a solve, or goes idle.  dxv: the Newton step just solved (A_ON_SOLVE),
 // left by the back substitution in the augmented matrix's last column
@@ -234,17 +269,7 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
         const long long path = (long long)idx;
         lsl[0] = path;
         lsl[S] = Ar.params ? (path / Ar.param_div) * Ar.H.nparam : -1;
-        if (Ar.starts) {
-          for (int v = 0; v < N; ++v) xes[v * S] = Ar.starts[path * N + v];
-        } else {
-          long long rem = Ar.first_index + path;
-          for (int v = N - 1; v >= 0; --v) {
-            const int d = Ar.deg[v];
-            const long long k = rem % d;
-            rem /= d;
-            xes[v * S] = Ar.roots[Ar.root_off[v] + (int)k];
-          }
-        }
+        load_start<N>(Ar, path, xes);
         DS_(D_TE) = 0.0;
         IS_(I_USED) = 0;
         IS_(I_FLAGS) = F_NEEDSCALE;
