@@ -32,6 +32,7 @@ if os.environ.get("NID_LU_UNFUSED"):
     FLAGS = FLAGS + ["-DNID_LU_UNFUSED"]
 if os.environ.get("NID_G10"):
     FLAGS = FLAGS + ["-DNID_G10=" + os.environ["NID_G10"]]
+    OBJ = OBJ + "_G" + os.environ["NID_G10"]
 # experiment variants: extra -D flags, objects in their own directory
 EXTRA = os.environ.get("NID_EXTRA_DEFS", "").split()
 if EXTRA:

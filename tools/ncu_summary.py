@@ -61,7 +61,7 @@ def main(rep, paths, outp):
         sys.stdout = old
     import os
     os.remove(tmp)
-    json.dump({"source": f"ncu --set full --clock-control none --import-source on -k regex:track_ctl -c 1, "
+    json.dump({"source": f"ncu --set full --clock-control none --import-source on -k regex:track_ -c 1, "
                          f"tools/probe_c5.py {paths} (C5 paths 0..{int(paths) - 1})",
                "metrics": m, "units": {k: units.get(k) for k in KEYS},
                "dram_bytes": dram, "dram_bytes_per_path": dram / float(paths),
