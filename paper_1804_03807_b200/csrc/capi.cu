@@ -48,6 +48,9 @@ struct NidHomotopy {
   double *acs, *act;
   int8_t* pslot;
   PTab* ptab = nullptr;  // host copy of the parameter-bank table (null: table too large / per-path params)
+  TermRec* rec = nullptr;  // streamed records (csrc/track_rec.cuh), n > 10
+  uint4* runs = nullptr;
+  int grun[17] = {0};
   cudaLibrary_t jit_lib = nullptr;  // NVRTC-specialised tracker (nid_homotopy_jit)
   cudaKernel_t jit_kernel = nullptr;
   HomDev dev() const {
@@ -71,6 +74,9 @@ struct NidHomotopy {
     h.act = act;
     h.pslot = pslot;
     h.gamma = gamma;
+    h.rec = rec;
+    h.runs = runs;
+    for (int v = 0; v <= 16; ++v) h.grun[v] = grun[v];
     return h;
   }
 };
@@ -320,6 +326,82 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
     }
     e = cudaMemcpy(h->fac, fac.data(), T * sizeof(uint4), cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(h->fex, fex.data(), T * sizeof(uint4), cudaMemcpyHostToDevice);
+    // streamed records for the large-system tracker (csrc/track_rec.cuh): per
+    // warp group, its rows in order, each row's terms grouped by factor count
+    // (stable), records contiguous; every term of total degree <= 12
+    bool rec_ok = n > 10;
+    for (int k = 0; k < T && rec_ok; ++k) {
+      int deg = 0;
+      for (int v = 0; v < n; ++v) deg += d->expo[k * NID_MAX_VARS + v];
+      if (deg > 12) rec_ok = false;
+    }
+    if (!e && rec_ok) {
+      const int G = rows::groups_for(n);
+      std::vector<TermRec> recs;
+      std::vector<uint4> runs;
+      recs.reserve(T + 16);
+      for (int gg = 0; gg <= 16; ++gg) h->grun[gg] = 0;
+      for (int gg = 0; gg < G; ++gg) {
+        h->grun[gg] = (int)runs.size();
+        for (int gi = h->goff[gg]; gi < h->goff[gg + 1]; ++gi) {
+          const int i = h->grow[gi];
+          std::vector<std::pair<int, int>> byk;  // (total degree, term)
+          for (int k = off[i]; k < off[i + 1]; ++k) {
+            int deg = 0;
+            for (int v = 0; v < n; ++v) deg += d->expo[k * NID_MAX_VARS + v];
+            byk.push_back({deg, k});
+          }
+          std::stable_sort(byk.begin(), byk.end(),
+                           [](const std::pair<int, int>& a, const std::pair<int, int>& b) { return a.first < b.first; });
+          if (byk.empty()) runs.push_back(make_uint4((unsigned)i, 0u, (unsigned)recs.size(), 0u));
+          for (size_t q = 0; q < byk.size();) {
+            size_t q1 = q;
+            while (q1 < byk.size() && byk[q1].first == byk[q].first) ++q1;
+            runs.push_back(make_uint4((unsigned)i, (unsigned)byk[q].first, (unsigned)recs.size(), (unsigned)(q1 - q)));
+            for (size_t z = q; z < q1; ++z) {
+              const int k = byk[z].second;
+              TermRec r;
+              memset(&r, 0, sizeof(r));
+              r.ctr = d->coef_target[2 * k];
+              r.cti = d->coef_target[2 * k + 1];
+              r.csr = d->coef_start[2 * k];
+              r.csi = d->coef_start[2 * k + 1];
+              r.acs = acs[k];
+              r.act = act[k];
+              unsigned long long meta = 0;
+              int npos = 0;
+              for (int v = 0; v < n; ++v)
+                for (int a = 0; a < d->expo[k * NID_MAX_VARS + v]; ++a) {
+                  meta |= (unsigned long long)v << (4 * npos);
+                  if (a > 0) meta |= 1ull << (52 + npos);
+                  ++npos;
+                }
+              meta |= (unsigned long long)npos << 48;
+              r.meta = meta;
+              r.pslot = d->param_slot ? (int)d->param_slot[k] : -1;
+              recs.push_back(r);
+            }
+            q = q1;
+          }
+        }
+      }
+      for (int gg = G; gg <= 16; ++gg) h->grun[gg] = (int)runs.size();
+      for (int z = 0; z < 16; ++z) {  // the ring reads up to two chunks past a group's end
+        TermRec r;
+        memset(&r, 0, sizeof(r));
+        recs.push_back(r);
+      }
+      e = cudaMalloc(&h->rec, recs.size() * sizeof(TermRec));
+      if (!e) e = cudaMemcpy(h->rec, recs.data(), recs.size() * sizeof(TermRec), cudaMemcpyHostToDevice);
+      if (!e) e = cudaMalloc(&h->runs, (runs.size() + 1) * sizeof(uint4));
+      if (!e && !runs.empty()) e = cudaMemcpy(h->runs, runs.data(), runs.size() * sizeof(uint4), cudaMemcpyHostToDevice);
+      if (e || getenv("NID_NO_REC")) {
+        cudaFree(h->rec);
+        cudaFree(h->runs);
+        h->rec = nullptr;
+        h->runs = nullptr;
+      }
+    }
   }
   if (!e && T) e = cudaMemcpy(h->cs, d->coef_start, T * sizeof(cd), cudaMemcpyHostToDevice);
   if (!e && T) e = cudaMemcpy(h->ct, d->coef_target, T * sizeof(cd), cudaMemcpyHostToDevice);
@@ -391,6 +473,8 @@ int nid_homotopy_destroy(NidHomotopy* h) {
   delete h->ptab;
   cudaFree(h->fac);
   cudaFree(h->fex);
+  if (h->rec) cudaFree(h->rec);
+  if (h->runs) cudaFree(h->runs);
   cudaFree(h->cs);
   cudaFree(h->ct);
   cudaFree(h->acs);

@@ -21,6 +21,17 @@
 #pragma once
 #include "nid_common.cuh"
 
+// One term of the streamed record table (track_rec.cuh), 64 bytes: target
+// and start coefficients, |ct|, |cs|, and the factor list -- 4 bits per
+// position (every variable once per unit of exponent, ascending), bits 48-51
+// the factor count K, bits 52-63 the repeat mask (bit j: position j repeats
+// position j-1's variable) -- and the per-path coefficient slot (-1: none).
+struct __align__(16) TermRec {
+  double ctr, cti, csr, csi, acs, act;
+  unsigned long long meta;
+  int pslot, pad;
+};
+
 struct HomDev {
   int n, nterms, nparam, maxdeg;
   int multilinear;        // every table exponent is 0 or 1
@@ -42,6 +53,12 @@ struct HomDev {
   const double* act;      // |ct|
   const int8_t* pslot;    // per-path target coefficient slot or null
   cd gamma;
+  // streamed records (n > 10, every term of total degree <= 12) or null:
+  // group g evaluates runs [grun[g], grun[g+1]) of `runs` = {row, factor
+  // count, first record, records}, whose records are contiguous
+  const TermRec* rec;
+  const uint4* runs;
+  int grun[17];
 };
 
 NID_D cd ldg_c(const cd* p) {

@@ -28,7 +28,7 @@ static int blocks_for(const void* fn, int threads, int smem = 0) {
 int CAT(launch_track_, NID_N)(const TrackArgs& a, int max_blocks, cudaStream_t s) {
   const void* fn = (const void*)track_ctl_kernel<NID_N>;
   const int threads = 32 * rows::groups<NID_N>();
-  const int smem = (int)ctl::Lay<NID_N>::bytes();
+  const int smem = (int)ctl::smem_bytes<NID_N>();
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int blocks = blocks_for(fn, threads, smem);
   long long need = (a.P + rows::SLOTS - 1) / rows::SLOTS;
@@ -93,6 +93,6 @@ int CAT(track_pt_regs_, NID_N)() {
 
 int CAT(track_threads_, NID_N)() { return rows::SLOTS; }  // path slots per block
 
-int CAT(track_smem_, NID_N)() { return (int)ctl::Lay<NID_N>::bytes(); }
+int CAT(track_smem_, NID_N)() { return (int)ctl::smem_bytes<NID_N>(); }
 
 }  // namespace nid

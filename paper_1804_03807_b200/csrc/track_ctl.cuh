@@ -28,6 +28,7 @@
 // min-norm fallback (solved by the controller lane on a global scratch copy).
 #pragma once
 #include "track_ptab.cuh"
+#include "track_rec.cuh"
 #include "track_rows.cuh"
 
 namespace ctl {
@@ -174,11 +175,22 @@ NID_D void lu_run(cd* augs, int q, bool solving, unsigned long long& perm, bool&
   if constexpr (MCK > 1) lu_run<N, G, CPW, MCK - 1>(augs, q, solving, perm, bad);
 }
 
+// dynamic shared memory of the tracker: the slot layout, plus (n > 10) each
+// warp's ring of streamed term records (track_rec.cuh)
+template <int N>
+constexpr size_t ring_bytes() {
+  return N > 10 ? (size_t)rows::groups<N>() * 2 * rec::CHUNK * sizeof(TermRec) : 0;
+}
+template <int N>
+constexpr size_t smem_bytes() {
+  return Lay<N>::bytes() + ring_bytes<N>();
+}
+
 // blocks per SM the register budget is sized for: as many as the shared
 // memory admits (228 KB per SM, 1 KB reserved per block), at most 3
 template <int N>
 constexpr int min_blocks() {
-  constexpr int fit = (int)((228u * 1024u) / (Lay<N>::bytes() + 1024u));
+  constexpr int fit = (int)((228u * 1024u) / (smem_bytes<N>() + 1024u));
   constexpr int cap = Lay<N>::G <= 4 ? 3 : 2;
   return fit < 1 ? 1 : (fit > cap ? cap : fit);
 }
@@ -577,6 +589,7 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
 // supplies a policy with the same signature whose rows are straight-line code.
 template <int N>
 struct TableEval {
+  static constexpr bool kTable = true;
   static NID_D void rows(const HomDev& H, int g, const cd (&x)[N], double t, const cd* prm, cd* aug, double* part,
                          bool want_scale, const cd* xs, double* axw) {
 #ifdef NID_EVAL_DENSE
@@ -585,6 +598,16 @@ struct TableEval {
     rows::eval_rows_fac<N>(H, g, xs, t, prm, aug, part, want_scale, axw);
 #endif
   }
+};
+
+// true for the table evaluator (the streamed-record path replaces it for n > 10)
+template <class E, class = void>
+struct has_table_flag {
+  static constexpr bool value = false;
+};
+template <class E>
+struct has_table_flag<E, decltype((void)E::kTable)> {
+  static constexpr bool value = true;
 };
 
 // Optional phase timers (-DNID_PHASE_TIMERS): per-warp clock64 cycles spent
@@ -662,7 +685,20 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     // ------------------------------------------------------------ evaluation
     if (!__syncthreads_or(W_IS(I_ACT) != A_IDLE)) break;
     NID_TP(1);  // barrier before the evaluation
-    if (W_IS(I_ACT) == A_EVAL) {
+    bool rec_done = false;
+    if constexpr (N > 10 && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value) {
+      if (Ar.H.rec) {  // streamed records: every lane of the warp takes part
+        const bool act = W_IS(I_ACT) == A_EVAL;
+        const bool want = act && (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
+        const long long pr = lb[S + lane];
+        const cd* prm = (act && pr >= 0) ? Ar.params + pr : nullptr;
+        TermRec* ring = reinterpret_cast<TermRec*>(smem_ctl + L::bytes()) + g * 2 * rec::CHUNK;
+        eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+                         db + L::AXW * S + lane, ring);
+        rec_done = true;
+      }
+    }
+    if (!rec_done && W_IS(I_ACT) == A_EVAL) {
       const bool want = (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
       if constexpr (ctl::is_ptab<Tab>::value) {
         PTEval<N>::rows(Ar.H, *tab, g, W_DS(D_TE), aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);

@@ -1,0 +1,196 @@
+// Streamed term-record evaluator of the table-driven tracker for large
+// systems (n > 10: C3/C4's 14-variable embedding, 4,068 terms).
+//
+// The table is too large for the parameter bank or L1, so every warp streams
+// its rows' terms from L2.  The host lays each warp group's terms out as one
+// contiguous run of 64-byte records (coefficients, |c|, factor list),
+// grouped per row by factor count (tracker row groups, capi.cu), and a warp
+// pulls them through a double-buffered ring in shared memory with cp.async:
+// 8 records (512 B, one 16-byte piece per lane) per chunk, the next chunk in
+// flight while the current one is evaluated -- the L2 latency is paid once
+// per 8 terms instead of once or twice per term.
+//
+// A term's factor list holds every variable once per unit of exponent
+// (x^2 y -> x, x, y), so every term is a product of K factors and the
+// partials are the leave-one-out products of polynomials.py:236-256
+// (`_StackedEvaluator`) with no exponent logic: for a repeated variable the
+// leave-one-out products of its positions sum to a * x^(a-1) * rest.  A
+// position that repeats the previous variable folds its partial into the
+// first position of the run, which alone updates the Jacobian entry.
+#pragma once
+#include "track_rows.cuh"
+
+namespace rec {
+
+using rows::SLOTS;
+
+constexpr int CHUNK = 8;  // records per chunk (32 lanes x 16 bytes)
+constexpr int KMAX = 12;  // factors per record
+
+NID_D unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// one chunk of records [r0, r0 + 8) into the ring slot `buf` (every lane one
+// 16-byte piece), committed as its own group
+NID_D void fetch(const TermRec* recs, long long r0, TermRec* buf, int lane) {
+  const char* src = reinterpret_cast<const char*>(recs + r0) + lane * 16;
+  const unsigned dst = smem_u32(reinterpret_cast<char*>(buf) + lane * 16);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+NID_D void wait_one() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// one term of factor count K, record `R` (in shared memory), at the slot's
+// point xs (|x| in axs); active lanes add into the slot's Jacobian row
+template <int N, int K>
+NID_D void term(const TermRec& R, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t,
+                const cd* prm, cd* row, bool active, cd& hv, double& sS, double& sT) {
+  const unsigned long long meta = R.meta;
+  cd ct = cd{R.ctr, R.cti};
+  if (R.pslot >= 0 && prm) ct = prm[R.pslot];
+  const cd c = td ? t * ct : alpha * cd{R.csr, R.csi} + t * ct;
+  int v[K > 0 ? K : 1];
+#pragma unroll
+  for (int j = 0; j < K; ++j) v[j] = (int)((meta >> (4 * j)) & 15);
+  cd Jv[K > 0 ? K : 1], X[K > 0 ? K : 1], P[K > 0 ? K : 1];
+#pragma unroll
+  for (int j = 0; j < K; ++j) Jv[j] = row[v[j] * SLOTS];
+  cd p = c;
+  double m = 1.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    X[j] = xs[v[j] * SLOTS];
+    P[j] = p;
+    p = p * X[j];
+    if (ws) m = __dmul_rn(m, axs[v[j] * SLOTS]);
+  }
+  hv = hv + p;
+  if (K > 0) {
+    const unsigned dup = (unsigned)(meta >> 52);
+    cd d[K > 0 ? K : 1];
+    cd s = cd{1.0, 0.0};
+#pragma unroll
+    for (int j = K - 1; j >= 0; --j) {
+      d[j] = (j == K - 1) ? P[j] : P[j] * s;
+      if (j > 0) s = (j == K - 1) ? X[j] : s * X[j];
+    }
+#pragma unroll
+    for (int j = K - 1; j > 0; --j)
+      if (dup & (1u << j)) d[j - 1] = d[j - 1] + d[j];
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (!(dup & (1u << j))) row[v[j] * SLOTS] = Jv[j] + d[j];
+    }
+  }
+  if (ws) {
+    if (!td) sS = __dadd_rn(sS, __dmul_rn(R.acs, m));
+    sT = __dadd_rn(sT, __dmul_rn(R.act, m));
+  }
+}
+
+}  // namespace rec
+
+// The rows of warp group g from the streamed records (same contract as
+// rows::eval_rows_fac).  Called by every lane of the warp (the ring needs all
+// 32 lanes); `active` lanes own an evaluating slot and alone write it.
+// ring: this warp's 2 x 8 records of shared memory.
+template <int N>
+NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const cd* prm, cd* aug, double* dbl,
+                         bool want_scale, bool active, double* axw, TermRec* ring) {
+  using L = rows::Layout<N>;
+  constexpr int S = rows::SLOTS;
+  const int lane = threadIdx.x & 31;
+  const cd alpha = (1.0 - t) * H.gamma;
+  const bool ws = __any_sync(0xffffffffu, want_scale && active);
+  const bool td = H.td != 0;
+  double r2 = 0.0, mS = 0.0, mT = 0.0;
+  const int u0 = H.grun[g], u1 = H.grun[g + 1];
+  if (u0 < u1) {
+    const long long base = __ldg(&H.runs[u0]).z;  // the group's first record
+    long long cnext = base;                        // next chunk to fetch
+    rec::fetch(H.rec, cnext, ring, lane);
+    cnext += rec::CHUNK;
+    rec::fetch(H.rec, cnext, ring + rec::CHUNK, lane);
+    cnext += rec::CHUNK;
+    long long kr = base;  // the next record to evaluate
+    int row_i = -1;
+    cd* row = aug;
+    cd hv = cd{0.0, 0.0};
+    double sS = 0.0, sT = 0.0;
+#pragma unroll 1
+    for (int u = u0; u <= u1; ++u) {
+      const uint4 run = u < u1 ? __ldg(&H.runs[u]) : make_uint4(0xffffffffu, 0u, 0u, 0u);
+      if ((int)run.x != row_i) {
+        if (row_i >= 0) {  // close the previous row: start system, -H, partial maxima
+          if (td) {  // G_i = x_i^{d_i} - 1 in closed form
+            const int d = H.tddeg[row_i];
+            const cd xi = xs[row_i * S];
+            cd q = cd{1.0, 0.0};
+#pragma unroll 1
+            for (int e = 1; e < d; ++e) q = q * xi;
+            hv = cfma(alpha, q * xi - cd{1.0, 0.0}, hv);
+            if (active) row[row_i * S] = row[row_i * S] + alpha * ((double)d * q);
+            if (ws) {
+              const double axi = axw[row_i * S];
+              double m = 1.0;
+#pragma unroll 1
+              for (int e = 0; e < d; ++e) m = __dmul_rn(m, axi);
+              sS = __dadd_rn(1.0, m);
+            }
+          }
+          if (active) row[N * S] = -hv;
+          r2 = nanmax(r2, cabs2(hv));
+          mS = fmax(mS, sS);
+          mT = fmax(mT, sT);
+        }
+        if (u == u1) break;
+        row_i = (int)run.x;
+        row = aug + row_i * (N + 1) * S;
+        if (active) {
+#pragma unroll
+          for (int v = 0; v < N; ++v) row[v * S] = cd{0.0, 0.0};
+        }
+        hv = cd{0.0, 0.0};
+        sS = 0.0;
+        sT = 0.0;
+      }
+      const int K = (int)run.y;
+      const long long kend = (long long)run.z + run.w;
+#pragma unroll 1
+      while (kr < kend) {
+        // the chunk holding kr has landed (the one after it may be in flight)
+        const int pos = (int)((kr - base) & (2 * rec::CHUNK - 1));
+        if ((pos & (rec::CHUNK - 1)) == 0) {
+          rec::wait_one();
+          __syncwarp();
+        }
+        const TermRec& R = ring[pos];
+        switch (K) {
+#define NID_RT(KK)                                                                                        \
+  case KK:                                                                                                \
+    rec::term<N, KK>(R, xs, axw, ws, td, alpha, t, prm, row, active, hv, sS, sT);                         \
+    break;
+          NID_RT(0) NID_RT(1) NID_RT(2) NID_RT(3) NID_RT(4) NID_RT(5) NID_RT(6) NID_RT(7) NID_RT(8)
+          NID_RT(9) NID_RT(10) NID_RT(11) NID_RT(12)
+#undef NID_RT
+          default:
+            break;
+        }
+        ++kr;
+        if (((kr - base) & (rec::CHUNK - 1)) == 0) {
+          // chunk done: every lane has read it, refill its slot two chunks ahead
+          __syncwarp();
+          rec::fetch(H.rec, cnext, ring + (((kr - base) - rec::CHUNK) & (2 * rec::CHUNK - 1)), lane);
+          cnext += rec::CHUNK;
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+  }
+  if (active) {
+    dbl[(L::R2 + g) * S] = r2;
+    dbl[(L::SS + g) * S] = mS;
+    dbl[(L::ST + g) * S] = mT;
+  }
+}
