@@ -46,7 +46,10 @@ NID_D void term(const TermRec& R, const cd* xs, const double* axs, bool ws, bool
                 const cd* prm, cd* row, bool active, cd& hv, double& sS, double& sT) {
   const unsigned long long meta = R.meta;
   cd ct = cd{R.ctr, R.cti};
-  if (R.pslot >= 0 && prm) ct = prm[R.pslot];
+  if (prm) {  // per-path coefficients (membership tests): warp-uniform test first
+    const int ps = R.pslot;
+    if (ps >= 0) ct = prm[ps];
+  }
   const cd c = td ? t * ct : alpha * cd{R.csr, R.csi} + t * ct;
   int v[K > 0 ? K : 1];
 #pragma unroll
@@ -73,18 +76,46 @@ NID_D void term(const TermRec& R, const cd* xs, const double* axs, bool ws, bool
       d[j] = (j == K - 1) ? P[j] : P[j] * s;
       if (j > 0) s = (j == K - 1) ? X[j] : s * X[j];
     }
+    if (K > 1 && dup) {  // repeated variables (uniform): fold into each run's first position
 #pragma unroll
-    for (int j = K - 1; j > 0; --j)
-      if (dup & (1u << j)) d[j - 1] = d[j - 1] + d[j];
-    if (active) {
+      for (int j = K - 1; j > 0; --j)
+        if (dup & (1u << j)) d[j - 1] = d[j - 1] + d[j];
+      if (active) {
 #pragma unroll
-      for (int j = 0; j < K; ++j)
-        if (!(dup & (1u << j))) row[v[j] * SLOTS] = Jv[j] + d[j];
+        for (int j = 0; j < K; ++j)
+          if (!(dup & (1u << j))) row[v[j] * SLOTS] = Jv[j] + d[j];
+      }
+    } else if (active) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) row[v[j] * SLOTS] = Jv[j] + d[j];
     }
   }
   if (ws) {
     if (!td) sS = __dadd_rn(sS, __dmul_rn(R.acs, m));
     sT = __dadd_rn(sT, __dmul_rn(R.act, m));
+  }
+}
+
+// the records [kr, kend) of one run (factor count K) through the ring:
+// wait for a chunk when the first of its records is reached, refill its
+// slot two chunks ahead once all of its records are consumed
+template <int N, int K>
+NID_D void run(const HomDev& H, long long base, long long& kr, long long kend, long long& cnext, TermRec* ring,
+               int lane, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, const cd* prm,
+               cd* row, bool active, cd& hv, double& sS, double& sT) {
+#pragma unroll 1
+  for (; kr < kend; ++kr) {
+    const int pos = (int)((kr - base) & (2 * CHUNK - 1));
+    if ((pos & (CHUNK - 1)) == 0) {  // the chunk holding kr has landed (the next may be in flight)
+      wait_one();
+      __syncwarp();
+    }
+    term<N, K>(ring[pos], xs, axs, ws, td, alpha, t, prm, row, active, hv, sS, sT);
+    if ((pos & (CHUNK - 1)) == CHUNK - 1) {  // chunk consumed by every lane: refill its slot
+      __syncwarp();
+      fetch(H.rec, cnext, ring + (pos & ~(CHUNK - 1)), lane);
+      cnext += CHUNK;
+    }
   }
 }
 
@@ -156,33 +187,17 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
       }
       const int K = (int)run.y;
       const long long kend = (long long)run.z + run.w;
-#pragma unroll 1
-      while (kr < kend) {
-        // the chunk holding kr has landed (the one after it may be in flight)
-        const int pos = (int)((kr - base) & (2 * rec::CHUNK - 1));
-        if ((pos & (rec::CHUNK - 1)) == 0) {
-          rec::wait_one();
-          __syncwarp();
-        }
-        const TermRec& R = ring[pos];
-        switch (K) {
-#define NID_RT(KK)                                                                                        \
-  case KK:                                                                                                \
-    rec::term<N, KK>(R, xs, axw, ws, td, alpha, t, prm, row, active, hv, sS, sT);                         \
+      switch (K) {
+#define NID_RT(KK)                                                                                       \
+  case KK:                                                                                               \
+    rec::run<N, KK>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm, row, active, hv, \
+                    sS, sT);                                                                             \
     break;
-          NID_RT(0) NID_RT(1) NID_RT(2) NID_RT(3) NID_RT(4) NID_RT(5) NID_RT(6) NID_RT(7) NID_RT(8)
-          NID_RT(9) NID_RT(10) NID_RT(11) NID_RT(12)
+        NID_RT(0) NID_RT(1) NID_RT(2) NID_RT(3) NID_RT(4) NID_RT(5) NID_RT(6) NID_RT(7) NID_RT(8)
+        NID_RT(9) NID_RT(10) NID_RT(11) NID_RT(12)
 #undef NID_RT
-          default:
-            break;
-        }
-        ++kr;
-        if (((kr - base) & (rec::CHUNK - 1)) == 0) {
-          // chunk done: every lane has read it, refill its slot two chunks ahead
-          __syncwarp();
-          rec::fetch(H.rec, cnext, ring + (((kr - base) - rec::CHUNK) & (2 * rec::CHUNK - 1)), lane);
-          cnext += rec::CHUNK;
-        }
+        default:
+          break;
       }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
