@@ -343,6 +343,7 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
       for (int gg = 0; gg <= 16; ++gg) h->grun[gg] = 0;
       for (int gg = 0; gg < G; ++gg) {
         h->grun[gg] = (int)runs.size();
+        const long long grp_base = (long long)recs.size();
         for (int gi = h->goff[gg]; gi < h->goff[gg + 1]; ++gi) {
           const int i = h->grow[gi];
           std::vector<std::pair<int, int>> byk;  // (total degree, term)
@@ -358,8 +359,42 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
             size_t q1 = q;
             while (q1 < byk.size() && byk[q1].first == byk[q].first) ++q1;
             runs.push_back(make_uint4((unsigned)i, (unsigned)byk[q].first, (unsigned)recs.size(), (unsigned)(q1 - q)));
-            for (size_t z = q; z < q1; ++z) {
-              const int k = byk[z].second;
+            // order the run so records at even offsets from the group's first
+            // record pair with a successor of disjoint variables (greedy, first
+            // fit within a window): the evaluator interleaves such pairs
+            std::vector<int> pend;
+            for (size_t z = q; z < q1; ++z) pend.push_back(byk[z].second);
+            auto vmask = [&](int k) {
+              unsigned mk = 0;
+              for (int v = 0; v < n; ++v)
+                if (d->expo[k * NID_MAX_VARS + v]) mk |= 1u << v;
+              return mk;
+            };
+            std::vector<std::pair<int, bool>> order;  // (term, paired with the next)
+            size_t gpos = recs.size() - (size_t)grp_base;
+            while (!pend.empty()) {
+              const int a = pend.front();
+              pend.erase(pend.begin());
+              bool paired = false;
+              if ((gpos & 1) == 0 && byk[q].first > 0 && byk[q].first <= 6) {  // rec::PAIRK
+                const unsigned ma = vmask(a);
+                for (size_t z = 0; z < pend.size() && z < 64; ++z)
+                  if (!(vmask(pend[z]) & ma)) {
+                    order.push_back({a, true});
+                    order.push_back({pend[z], false});
+                    pend.erase(pend.begin() + z);
+                    paired = true;
+                    gpos += 2;
+                    break;
+                  }
+              }
+              if (!paired) {
+                order.push_back({a, false});
+                gpos += 1;
+              }
+            }
+            for (size_t z = 0; z < order.size(); ++z) {
+              const int k = order[z].first;
               TermRec r;
               memset(&r, 0, sizeof(r));
               r.ctr = d->coef_target[2 * k];
@@ -377,6 +412,7 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
                   ++npos;
                 }
               meta |= (unsigned long long)npos << 48;
+              if (order[z].second) meta |= 1ull << 52;  // paired with the next record
               r.meta = meta;
               r.pslot = d->param_slot ? (int)d->param_slot[k] : -1;
               recs.push_back(r);

@@ -26,6 +26,7 @@ using rows::SLOTS;
 
 constexpr int CHUNK = 8;  // records per chunk (32 lanes x 16 bytes)
 constexpr int KMAX = 12;  // factors per record
+constexpr int PAIRK = 6;  // terms of at most this many factors are paired (register budget)
 
 NID_D unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -39,61 +40,108 @@ NID_D void fetch(const TermRec* recs, long long r0, TermRec* buf, int lane) {
 }
 NID_D void wait_one() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-// one term of factor count K, record `R` (in shared memory), at the slot's
-// point xs (|x| in axs); active lanes add into the slot's Jacobian row
+// One term of factor count K, record `R` (in shared memory), at the slot's
+// point xs (|x| in axs), in three phases so two terms with disjoint
+// variables can be interleaved (term2): load (coefficient, Jacobian entries,
+// point), compute (prefix products, leave-one-out partials, repeat folding),
+// commit (active lanes add into the slot's Jacobian row).
+template <int K>
+struct TermState {
+  static constexpr int KK = K > 0 ? K : 1;
+  int v[KK];
+  cd Jv[KK], X[KK], d[KK];
+  cd p;
+  double m;
+  unsigned dup;
+  double acs, act;
+};
+
 template <int N, int K>
-NID_D void term(const TermRec& R, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t,
-                const cd* prm, cd* row, bool active, cd& hv, double& sS, double& sT) {
+NID_D void t_load(TermState<K>& S, const TermRec& R, const cd* xs, const double* axs, bool ws, bool td, cd alpha,
+                  double t, const cd* prm, const cd* row) {
   const unsigned long long meta = R.meta;
   cd ct = cd{R.ctr, R.cti};
   if (prm) {  // per-path coefficients (membership tests): warp-uniform test first
     const int ps = R.pslot;
     if (ps >= 0) ct = prm[ps];
   }
-  const cd c = td ? t * ct : alpha * cd{R.csr, R.csi} + t * ct;
-  int v[K > 0 ? K : 1];
+  S.p = td ? t * ct : alpha * cd{R.csr, R.csi} + t * ct;  // the coefficient heads the prefix chain
+  S.dup = (unsigned)(meta >> 52) & ~1u;                    // bit 0: the pairing flag, not a repeat
+  S.acs = R.acs;
+  S.act = R.act;
+  S.m = 1.0;
 #pragma unroll
-  for (int j = 0; j < K; ++j) v[j] = (int)((meta >> (4 * j)) & 15);
-  cd Jv[K > 0 ? K : 1], X[K > 0 ? K : 1], P[K > 0 ? K : 1];
+  for (int j = 0; j < K; ++j) S.v[j] = (int)((meta >> (4 * j)) & 15);
 #pragma unroll
-  for (int j = 0; j < K; ++j) Jv[j] = row[v[j] * SLOTS];
-  cd p = c;
-  double m = 1.0;
+  for (int j = 0; j < K; ++j) S.Jv[j] = row[S.v[j] * SLOTS];
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    X[j] = xs[v[j] * SLOTS];
-    P[j] = p;
-    p = p * X[j];
-    if (ws) m = __dmul_rn(m, axs[v[j] * SLOTS]);
+    S.X[j] = xs[S.v[j] * SLOTS];
+    if (ws) S.m = __dmul_rn(S.m, axs[S.v[j] * SLOTS]);
   }
-  hv = hv + p;
-  if (K > 0) {
-    const unsigned dup = (unsigned)(meta >> 52);
-    cd d[K > 0 ? K : 1];
-    cd s = cd{1.0, 0.0};
+}
+
+template <int K>
+NID_D void t_compute(TermState<K>& S) {
+  cd P[TermState<K>::KK];
+  cd p = S.p;
 #pragma unroll
-    for (int j = K - 1; j >= 0; --j) {
-      d[j] = (j == K - 1) ? P[j] : P[j] * s;
-      if (j > 0) s = (j == K - 1) ? X[j] : s * X[j];
+  for (int j = 0; j < K; ++j) {
+    P[j] = p;
+    p = p * S.X[j];
+  }
+  S.p = p;  // the term's value
+  cd s = cd{1.0, 0.0};
+#pragma unroll
+  for (int j = K - 1; j >= 0; --j) {
+    S.d[j] = (j == K - 1) ? P[j] : P[j] * s;
+    if (j > 0) s = (j == K - 1) ? S.X[j] : s * S.X[j];
+  }
+}
+
+template <int K>
+NID_D void t_commit(TermState<K>& S, cd* row, bool active, bool ws, bool td, cd& hv, double& sS, double& sT) {
+  hv = hv + S.p;
+  if (K > 1 && S.dup) {  // repeated variables (uniform): fold into each run's first position
+#pragma unroll
+    for (int j = K - 1; j > 0; --j)
+      if (S.dup & (1u << j)) S.d[j - 1] = S.d[j - 1] + S.d[j];
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (!(S.dup & (1u << j))) row[S.v[j] * SLOTS] = S.Jv[j] + S.d[j];
     }
-    if (K > 1 && dup) {  // repeated variables (uniform): fold into each run's first position
+  } else if (active) {
 #pragma unroll
-      for (int j = K - 1; j > 0; --j)
-        if (dup & (1u << j)) d[j - 1] = d[j - 1] + d[j];
-      if (active) {
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-          if (!(dup & (1u << j))) row[v[j] * SLOTS] = Jv[j] + d[j];
-      }
-    } else if (active) {
-#pragma unroll
-      for (int j = 0; j < K; ++j) row[v[j] * SLOTS] = Jv[j] + d[j];
-    }
+    for (int j = 0; j < K; ++j) row[S.v[j] * SLOTS] = S.Jv[j] + S.d[j];
   }
   if (ws) {
-    if (!td) sS = __dadd_rn(sS, __dmul_rn(R.acs, m));
-    sT = __dadd_rn(sT, __dmul_rn(R.act, m));
+    if (!td) sS = __dadd_rn(sS, __dmul_rn(S.acs, S.m));
+    sT = __dadd_rn(sT, __dmul_rn(S.act, S.m));
   }
+}
+
+template <int N, int K>
+NID_D void term(const TermRec& R, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t,
+                const cd* prm, cd* row, bool active, cd& hv, double& sS, double& sT) {
+  TermState<K> A;
+  t_load<N, K>(A, R, xs, axs, ws, td, alpha, t, prm, row);
+  t_compute<K>(A);
+  t_commit<K>(A, row, active, ws, td, hv, sS, sT);
+}
+
+// two terms whose variable sets are disjoint (paired on the host): every
+// load first, the two product chains interleaved, then both commits
+template <int N, int K>
+NID_D void term2(const TermRec& RA, const TermRec& RB, const cd* xs, const double* axs, bool ws, bool td, cd alpha,
+                 double t, const cd* prm, cd* row, bool active, cd& hv, double& sS, double& sT) {
+  TermState<K> A, B;
+  t_load<N, K>(A, RA, xs, axs, ws, td, alpha, t, prm, row);
+  t_load<N, K>(B, RB, xs, axs, ws, td, alpha, t, prm, row);
+  t_compute<K>(A);
+  t_compute<K>(B);
+  t_commit<K>(A, row, active, ws, td, hv, sS, sT);
+  t_commit<K>(B, row, active, ws, td, hv, sS, sT);
 }
 
 // the records [kr, kend) of one run (factor count K) through the ring:
@@ -104,16 +152,24 @@ NID_D void run(const HomDev& H, long long base, long long& kr, long long kend, l
                int lane, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, const cd* prm,
                cd* row, bool active, cd& hv, double& sS, double& sT) {
 #pragma unroll 1
-  for (; kr < kend; ++kr) {
+  while (kr < kend) {
     const int pos = (int)((kr - base) & (2 * CHUNK - 1));
     if ((pos & (CHUNK - 1)) == 0) {  // the chunk holding kr has landed (the next may be in flight)
       wait_one();
       __syncwarp();
     }
-    term<N, K>(ring[pos], xs, axs, ws, td, alpha, t, prm, row, active, hv, sS, sT);
-    if ((pos & (CHUNK - 1)) == CHUNK - 1) {  // chunk consumed by every lane: refill its slot
+    // a record at an even offset flagged as paired (meta bit 52) shares no
+    // variable with its successor in the same run (capi.cu)
+    if (K > 0 && K <= PAIRK && ((ring[pos].meta >> 52) & 1ull)) {
+      term2<N, (K <= PAIRK ? K : 1)>(ring[pos], ring[pos + 1], xs, axs, ws, td, alpha, t, prm, row, active, hv, sS, sT);
+      kr += 2;
+    } else {
+      term<N, K>(ring[pos], xs, axs, ws, td, alpha, t, prm, row, active, hv, sS, sT);
+      kr += 1;
+    }
+    if (((kr - base) & (CHUNK - 1)) == 0) {  // chunk consumed by every lane: refill its slot
       __syncwarp();
-      fetch(H.rec, cnext, ring + (pos & ~(CHUNK - 1)), lane);
+      fetch(H.rec, cnext, ring + ((pos & ~(CHUNK - 1))), lane);
       cnext += CHUNK;
     }
   }
