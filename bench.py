@@ -8,9 +8,10 @@ star): C5, the n=10 cyclic-support system, total-degree homotopy, 10! =
 3,628,800 paths.  One step = every path tracked t: 0 -> 1 with the
 reference's TrackParams, endpoints finished (damped Newton, SVD condition,
 double-double polish of ill-conditioned ones), and -- for N > 1 -- the finite
-endpoints gathered to rank 0 over NCCL.  Ranks own equal contiguous shards of
-the path index space (strong scaling: total work fixed) and generate their
-own starts on the device.
+endpoints gathered to rank 0 over NCCL.  Rank r owns the strided shard r, r+N,
+r+2N, ... of the path index space (strong scaling: total work fixed; a
+uniform sample per rank, so shards carry equal work) and generates its own
+starts on the device.
 
 value : paths/s with everything device-resident (CUDA events on the stream,
         max over ranks).
@@ -164,8 +165,7 @@ def native_arm(args, prob):
     dev = torch.device("cuda", ctx.local_rank)
     n = prob.n
     P = prob.paths
-    lo, hi = ctx.shard(P)
-    Pl = hi - lo
+    lo, stride, Pl = ctx.shard_strided(P)  # rank r: path indices r, r + N, ... (balanced work)
     h = LinearHomotopy(prob.start, prob.target, prob.gamma)
     params = TrackParams()
     fm = flops.flop_model(h.lowered())
@@ -186,7 +186,7 @@ def native_arm(args, prob):
     def step():
         flush.fill_(1.0)
         c = tracker.track_batch_device(h, params, Pl, outp, degrees=prob.degrees, first_index=lo,
-                                       stream=stream.cuda_stream, jit=args.jit)
+                                       index_stride=stride, stream=stream.cuda_stream, jit=args.jit)
         if ctx.world > 1:
             gather_finite(ctx, x_end, status)
         return c
@@ -230,7 +230,7 @@ def native_arm(args, prob):
         from paper_1804_03807_b200 import systems
 
         X0 = torch.empty((Pl, n, 2), dtype=torch.float64).pin_memory()
-        X0.numpy().view(np.complex128).reshape(Pl, n)[:] = systems.total_degree_starts(prob.degrees, lo, Pl)
+        X0.numpy().view(np.complex128).reshape(Pl, n)[:] = systems.total_degree_starts(prob.degrees, lo, Pl, stride)
         pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory()  # noqa: E731
         ho = tracker.TrackResults(pin((Pl, n, 2), torch.float64).numpy().view(np.complex128).reshape(Pl, n),
                                   pin(Pl, torch.int8).numpy(), pin(Pl, torch.int32).numpy(),

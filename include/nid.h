@@ -136,6 +136,15 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
                     long long first_index, const int32_t* degrees, const double* params,
                     int param_div, NidPathOut* out, int device_io, void* stream);
 
+/* nid_track_batch with total-degree start path indices first_index + i * index_stride
+ * (i < P): a rank's strided share of the path index space (multi-GPU sharding,
+ * work_crew's job list split across processes, parallel.py:69-109).
+ * nid_track_batch is the index_stride == 1 case. */
+int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
+                            long long first_index, long long index_stride, const int32_t* degrees,
+                            const double* params, int param_div, NidPathOut* out, int device_io,
+                            void* stream);
+
 int nid_last_counters(NidCounters* c);
 
 /* Compile a homotopy-specialised tracker with NVRTC and attach it to h:

@@ -543,7 +543,16 @@ enum {
 int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
                     long long first_index, const int32_t* degrees, const double* params, int param_div,
                     NidPathOut* out, int device_io, void* stream) {
+  return nid_track_batch_strided(h, prm, P, starts, first_index, 1, degrees, params, param_div, out, device_io,
+                                 stream);
+}
+
+int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
+                            long long first_index, long long index_stride, const int32_t* degrees,
+                            const double* params, int param_div, NidPathOut* out, int device_io,
+                            void* stream) {
   if (!h || !prm || !out) FAIL("null argument");
+  if (index_stride < 1) FAIL("index_stride must be >= 1");
   if (P < 0) FAIL("negative path count");
   const int n = h->n;
   cudaStream_t s = (cudaStream_t)stream;
@@ -605,6 +614,7 @@ int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
   a.prm = *prm;
   a.P = P;
   a.first_index = first_index;
+  a.index_stride = index_stride;
   a.starts = d_starts;
   for (int v = 0; v < NID_MAX_VARS; ++v) a.deg[v] = (degrees && v < n) ? degrees[v] : 1;
   if (!starts) {

@@ -9,6 +9,7 @@ struct TrackArgs {
   NidTrackParams prm;
   long long P;            // paths in this launch
   long long first_index;  // total-degree start index of path 0
+  long long index_stride; // start index of path i: first_index + i * index_stride
   const cd* starts;       // [P][n] or null for total-degree starts
   int deg[NID_MAX_VARS];  // total-degree start degrees
   int root_off[NID_MAX_VARS];  // offsets of each variable's roots of unity in `roots`

@@ -228,7 +228,7 @@ __device__ NID_CLAIM_ATTR void load_start(const TrackArgs& Ar, long long path, c
   if (Ar.starts) {
     for (int v = 0; v < N; ++v) xes[v * S] = Ar.starts[path * N + v];
   } else {
-    long long rem = Ar.first_index + path;
+    long long rem = Ar.first_index + path * Ar.index_stride;
     if (rem < (1ll << 32)) {  // 32-bit digits (every config here)
       unsigned r32 = (unsigned)rem;
       for (int v = N - 1; v >= 0; --v) {

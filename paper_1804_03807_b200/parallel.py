@@ -25,6 +25,16 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def shard_strided(total: int, rank: int, world: int) -> tuple[int, int, int]:
+    """Strided shard (first, stride, count): rank r owns path indices r, r + world,
+    r + 2 world, ... -- a uniform sample of the index space, so ranks get equal
+    work even where path cost varies along the index order (contiguous C5
+    shards differ by 5 % in work, tools/probe_shards.py)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return rank, world, (int(total) - rank + world - 1) // world
+
+
 @dataclass
 class DistContext:
     rank: int = 0
@@ -58,6 +68,9 @@ class DistContext:
 
     def shard(self, total: int) -> tuple[int, int]:
         return shard_range(total, self.rank, self.world)
+
+    def shard_strided(self, total: int) -> tuple[int, int, int]:
+        return shard_strided(total, self.rank, self.world)
 
     def _device(self):
         import torch

@@ -122,12 +122,13 @@ _FOREIGN: dict = {}
 
 
 def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=None, first_index: int = 0,
-                count: int | None = None, target_params=None, param_div: int = 1,
+                count: int | None = None, index_stride: int = 1, target_params=None, param_div: int = 1,
                 out: TrackResults | None = None, jit: bool | None = None) -> TrackResults:
     """Track many paths of h in one launch.
 
     starts: [P, n] start points, or None with `degrees` for total-degree
-    starts generated on the device for path indices [first_index, first_index+count).
+    starts generated on the device for path indices first_index + i * index_stride,
+    i < count.
     target_params: per-path target coefficients ([P/param_div, nparam]) for
     homotopies lowered with parameter slots (membership tests)."""
     L = _lib.lib()
@@ -153,8 +154,9 @@ def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=
     o = _lib.PathOutC(_lib.ptr(out.x), _lib.ptr(out.status), _lib.ptr(out.steps), _lib.ptr(out.t_reached),
                       _lib.ptr(out.residual), _lib.ptr(out.condition), _lib.ptr(out.regular))
     pc = params.to_c()
-    _lib.check(L.nid_track_batch(dev.handle, C.byref(pc), P, _lib.ptr(st), int(first_index), _lib.ptr(deg),
-                                 _lib.ptr(prm), int(param_div), C.byref(o), 0, None), L)
+    _lib.check(L.nid_track_batch_strided(dev.handle, C.byref(pc), P, _lib.ptr(st), int(first_index),
+                                         int(index_stride), _lib.ptr(deg), _lib.ptr(prm), int(param_div),
+                                         C.byref(o), 0, None), L)
     out.counters = _lib.last_counters()
     return out
 
@@ -281,12 +283,13 @@ def classify(coords, n_original: int, infinity_threshold: float = 1e8, zero_tol:
 
 
 def track_batch_device(h, params: TrackParams, P: int, out: dict, *, degrees=None, first_index: int = 0,
-                       starts_ptr: int = 0, params_ptr: int = 0, param_div: int = 1, stream: int = 0,
-                       jit: bool | None = None) -> dict:
+                       index_stride: int = 1, starts_ptr: int = 0, params_ptr: int = 0, param_div: int = 1,
+                       stream: int = 0, jit: bool | None = None) -> dict:
     """Device-resident variant of `track_batch`: every buffer is a device
     pointer (e.g. torch CUDA tensors' data_ptr()), nothing is copied, and the
     kernels run on `stream`.  `out` maps x_end/status/steps/t_reached/
-    residual/condition/regular to device pointers."""
+    residual/condition/regular to device pointers.  Total-degree starts are
+    the path indices first_index + i * index_stride (a rank's strided shard)."""
     L = _lib.lib()
     dev = _device_of(h)
     if want_jit(dev, P, jit):
@@ -295,7 +298,8 @@ def track_batch_device(h, params: TrackParams, P: int, out: dict, *, degrees=Non
     o = _lib.PathOutC(out["x_end"], out["status"], out["steps"], out["t_reached"], out["residual"],
                       out["condition"], out["regular"])
     pc = params.to_c()
-    _lib.check(L.nid_track_batch(dev.handle, C.byref(pc), int(P), C.c_void_p(starts_ptr or None),
-                                 int(first_index), _lib.ptr(deg), C.c_void_p(params_ptr or None), int(param_div),
-                                 C.byref(o), 1, C.c_void_p(stream or None)), L)
+    _lib.check(L.nid_track_batch_strided(dev.handle, C.byref(pc), int(P), C.c_void_p(starts_ptr or None),
+                                         int(first_index), int(index_stride), _lib.ptr(deg),
+                                         C.c_void_p(params_ptr or None), int(param_div), C.byref(o), 1,
+                                         C.c_void_p(stream or None)), L)
     return _lib.last_counters()

@@ -98,6 +98,22 @@ def test_track_c2_full_5040(nid):
     print("C2 status agreement", agree, res.counts(), res.counters)
 
 
+def test_track_strided_shards_partition_c2(nid):
+    """Strided shards (multi-GPU sharding, rank r: indices r, r+W, ...) track
+    exactly the paths of the contiguous launch: same statuses and endpoints."""
+    p = configs.c2()
+    h = gpu_h(p)
+    full = tracker.track_batch(h, None, degrees=p.degrees, count=p.paths)
+    W = 3
+    for r in range(W):
+        sh = tracker.track_batch(h, None, degrees=p.degrees, first_index=r, index_stride=W,
+                                 count=(p.paths - r + W - 1) // W)
+        idx = np.arange(r, p.paths, W)
+        assert np.array_equal(sh.status, full.status[idx])
+        fin = np.isin(sh.status, (0, 2))
+        assert np.array_equal(sh.x[fin], full.x[idx][fin])
+
+
 def test_track_c5_sample(nid):
     p = configs.c5()
     fix = golden("track_c5_sample")

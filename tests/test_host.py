@@ -145,6 +145,28 @@ def test_shard_range_covers_exactly(total, world):
     assert max(sizes) - min(sizes) <= 1
 
 
+@pytest.mark.parametrize("total,world", [(3628800, 8), (5040, 3), (7, 4), (0, 2)])
+def test_shard_strided_partitions(total, world):
+    got = []
+    for r in range(world):
+        first, stride, count = parallel.shard_strided(min(total, 100000), r, world)
+        got.append(first + stride * np.arange(count))
+    allidx = np.sort(np.concatenate(got)) if got else np.array([])
+    assert np.array_equal(allidx, np.arange(min(total, 100000)))
+    sizes = [len(g) for g in got]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_strided_total_degree_starts_are_a_subset():
+    from paper_1804_03807_b200 import systems
+
+    deg = [1, 2, 3, 4]
+    full = systems.total_degree_starts(deg)
+    for r in range(3):
+        sub = systems.total_degree_starts(deg, r, None, 3)
+        assert np.array_equal(sub, full[r::3])
+
+
 def _gloo_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                       LOCAL_RANK=str(rank))
