@@ -57,3 +57,22 @@ def test_c4_membership_matches_construction(c3_top):
     d = len(lv.zero_slack)
     assert 0 < tracked <= d * len(cands) and tracked % d == 0
     assert np.all((verdict == 1) == (labels == 1))
+
+
+def test_c4_hard_candidates_match_oracle(nid):
+    """The full 100,000-candidate C4 batch on a B200 disagreed with the
+    construction labels on 4 candidates (3 on-component points reported off
+    it, 1 indeterminate).  The CPU oracle (the pinned restatement of
+    nidpipe.filtering.membership_test) reaches the same verdicts from the same
+    witness points (tests/golden/make_c4_hard.py): these are the reference's
+    answers, not GPU errors.  The GPU must reproduce the oracle exactly on
+    them and on six agreeing controls."""
+    from conftest import golden
+    from paper_1804_03807_b200.tracker import Solution
+
+    g = golden("c4_hard")
+    pd = configs.c3()
+    pts = [Solution(w, 0.0, 1.0) for w in g["witness"]]
+    W = filtering.WitnessSet(pd.emb.k, pd.emb, pts)
+    verdict, _ = filtering.membership_batch(W, g["candidates"])
+    assert np.array_equal(verdict, g["oracle_verdict"]), (verdict, g["oracle_verdict"], g["labels"])
