@@ -37,7 +37,7 @@ def main(csvp, ctl_src="paper_1804_03807_b200/csrc/track_ctl.cuh"):
     for i, l in enumerate(open(ctl_src), 1):
         if "void track_body(" in l:
             ctl_fn_end = i
-        if "NID_D void lu_step" in l and lu_lo is None:
+        if ("NID_D int lu_pivot" in l or "NID_D void lu_step" in l) and lu_lo is None:
             lu_lo = i
         if "// blocks per SM" in l:
             lu_hi = i
