@@ -18,6 +18,8 @@
  *   nid_track_batch       work_crew(jobs, p, lambda x0: track(h, x0))  parallel.py:69-109,
  *                         track / _correct / _finish / _damped_newton  tracker.py:184-407
  *                         _endpoint_solution / _dd_polish              tracker.py:255-302
+ *   nid_track_batch_strided  the same over a rank's strided share of the
+ *                         start-path indices (one process per GPU)     parallel.py:69-109
  *   nid_refine_batch      newton_refine + classify                     tracker.py:410-455
  *   nid_dd_refine_batch   refine_dd                                    tracker.py:431-435
  *   nid_match_pairs       points_match over all pairs (for _dedup)     filtering.py:73-78,140-150
