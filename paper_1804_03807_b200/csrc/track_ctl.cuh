@@ -200,94 +200,6 @@ NID_D void lu_run(cd* augs, int q, bool solving, unsigned long long& perm, bool&
   if constexpr (MCK > 1) lu_run<N, G, CPW, MCK - 1>(augs, q, solving, perm, bad, pk);
 }
 
-// Two elimination steps k, k+1 in one pass over the trailing rows (a blocked
-// right-looking LU with block size 2, zgetf2's pivot order): column k+1 is
-// brought up to date first (its rows split over the slot's G lanes, each
-// storing its rows' step-k multipliers in the dead column k), step k+1's
-// pivot is chosen on it, and every trailing entry then takes both rank-1
-// updates in one read-modify-write -- half the shared-memory traffic of two
-// single steps, which is what bounds the LU.  MC2 = ceil((N-k-1)/G): the
-// trailing columns j >= k+2 a lane owns (j == k+2+q mod G).
-template <int N, int G, int CPW, int MC2>
-NID_D void lu_step2(cd* augs, int k, int q, bool solving, unsigned long long& perm, bool& bad) {
-  constexpr int SL = rows::SLOTS;
-  // step k: pivot, multipliers of column k and the update of column k+1
-  const int r0 = perm_swap(perm, k, lu_pivot<N, G, CPW, MC2 + 1>(augs, k, q, perm, bad));
-  const cd inv0 = crecip_fast(rows::A<N>(augs, r0, k));
-  const cd p01 = rows::A<N>(augs, r0, k + 1);
-  if (solving) {
-#pragma unroll
-    for (int m = 0; m < MC2; ++m) {
-      const int pos = k + 1 + q + m * G;
-      if (pos < N) {
-        const int r = (perm >> (4 * pos)) & 15;
-        cd* const rp = &rows::A<N>(augs, r, 0);
-        const cd l0 = lu_mul(rp[k * SL], inv0);
-        rp[(k + 1) * SL] = lu_upd(rp[(k + 1) * SL], l0, p01);
-        rp[k * SL] = l0;  // column k is dead after step k: keep the multiplier
-      }
-    }
-  }
-  __syncwarp();
-  // step k+1: pivot on the updated column k+1
-  const int r1 = perm_swap(perm, k + 1, lu_pivot<N, G, CPW, MC2>(augs, k + 1, q, perm, bad));
-  const cd inv1 = crecip_fast(rows::A<N>(augs, r1, k + 1));
-  // the two pivot rows over the lane's trailing columns (column slots past
-  // the last column read column N: written unconditionally, unused)
-  const int j0 = k + 2 + q;
-  const cd l0r1 = rows::A<N>(augs, r1, k);
-  cd prow0[MC2], prow1[MC2];
-#pragma unroll
-  for (int m = 0; m < MC2; ++m) {
-    const int j = min(j0 + m * G, N);
-    prow0[m] = rows::A<N>(augs, r0, j);
-    prow1[m] = lu_upd(rows::A<N>(augs, r1, j), l0r1, prow0[m]);
-  }
-  if (solving) {
-    const bool lastok = j0 + (MC2 - 1) * G <= N;  // only the last column slot can fall off the end
-#pragma unroll
-    for (int m = 0; m < MC2; ++m)
-      if (m < MC2 - 1 || lastok) rows::A<N>(augs, r1, j0 + m * G) = prow1[m];
-#pragma unroll 1
-    for (int pos = k + 2; pos < N; ++pos) {
-      const int r = (perm >> (4 * pos)) & 15;
-      cd* const rp = &rows::A<N>(augs, r, 0);
-      const cd l0 = rp[k * SL];
-      const cd l1 = lu_mul(rp[(k + 1) * SL], inv1);
-#pragma unroll
-      for (int m = 0; m < MC2; ++m)
-        if (m < MC2 - 1 || lastok) {
-          cd& a = rp[(j0 + m * G) * SL];
-          a = lu_upd(lu_upd(a, l0, prow0[m]), l1, prow1[m]);
-        }
-    }
-  }
-  __syncwarp();
-  // the pivots' reciprocals replace them (the back substitution multiplies)
-  if (solving && q == 0) {
-    rows::A<N>(augs, r0, k) = inv0;
-    rows::A<N>(augs, r1, k + 1) = inv1;
-  }
-  __syncwarp();
-}
-
-// the pairs k = 0, 2, 4, ... (k+1 < N) split into runs of equal
-// MC2 = ceil((N-k-1)/G); an odd N ends with the single step k = N-1
-template <int N, int G, int CPW, int MC2>
-NID_D void lu_run2(cd* augs, int q, bool solving, unsigned long long& perm, bool& bad) {
-  constexpr int kb0 = N - 1 - MC2 * G > 0 ? N - 1 - MC2 * G : 0;
-  constexpr int kb = (kb0 + 1) & ~1;          // first even k with ceil((N-k-1)/G) == MC2
-  constexpr int ke = N - 1 - (MC2 - 1) * G;   // one past the last
-#pragma unroll 1
-  for (int k = kb; k < ke && k + 1 < N; k += 2) lu_step2<N, G, CPW, MC2>(augs, k, q, solving, perm, bad);
-  if constexpr (MC2 > 1) {
-    lu_run2<N, G, CPW, MC2 - 1>(augs, q, solving, perm, bad);
-  } else if constexpr (N % 2 == 1) {
-    int pk = lu_pivot<N, G, CPW, 1>(augs, N - 1, q, perm, bad);
-    lu_step<N, G, CPW, 1>(augs, N - 1, q, solving, perm, bad, pk);
-  }
-}
-
 // dynamic shared memory of the tracker: the slot layout, plus (n > 10) each
 // warp's ring of streamed term records (track_rec.cuh)
 template <int N>
@@ -890,17 +802,8 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
 #pragma unroll
         for (int i = 0; i < N; ++i) perm |= (unsigned long long)i << (4 * i);
         bool bad = false;
-#ifdef NID_LU_BLOCK2
-        if constexpr (N >= 2) {
-          lu_run2<N, G, CPW, (N - 1 + G - 1) / G>(augs, q, solving, perm, bad);
-        } else {
-          int pk = lu_pivot<N, G, CPW, 1>(augs, 0, q, perm, bad);
-          lu_run<N, G, CPW, 1>(augs, q, solving, perm, bad, pk);
-        }
-#else
         int pk = lu_pivot<N, G, CPW, (N + G - 1) / G>(augs, 0, q, perm, bad);
         lu_run<N, G, CPW, (N + G - 1) / G>(augs, q, solving, perm, bad, pk);
-#endif
         if (solving && q == 0) {
           lb[2 * S + ss] = (long long)perm;
           ib[I_BAD * S + ss] = bad ? 1 : 0;

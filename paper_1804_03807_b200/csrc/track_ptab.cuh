@@ -57,11 +57,7 @@ template <int N, int K, bool ML>
 NID_D void run(const PTab& T, int r, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, cd* row,
                cd& hv, double& sS, double& sT) {
   const int k0 = T.run_k0[r], cnt = T.run_n[r], f0 = T.run_f0[r];
-#ifndef NID_PT_UNROLL_K
-#define NID_PT_UNROLL_K 0
-#endif
-  constexpr int UNR = K <= NID_PT_UNROLL_K ? 2 : 1;
-#pragma unroll UNR
+#pragma unroll 1
   for (int j = 0; j < cnt; ++j) {
     const int k = k0 + j, fb = f0 + j * K;
     const cd ct = T.ct[k];
