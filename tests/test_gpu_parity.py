@@ -196,3 +196,22 @@ def test_track_c5_large_sample(nid):
     xg = res.x[fin_gpu]
     d = np.max(np.abs(xg - fix["fin_x"]), axis=1) / np.maximum(1.0, np.max(np.abs(fix["fin_x"]), axis=1))
     assert np.all(d < 1e-8), d.max()
+
+
+@pytest.mark.parametrize("n", [11, 13, 16])
+def test_large_dense_quadrics_match_oracle(nid, n):
+    """Systems of 11..16 variables (dense random quadrics: 78..153 terms a row,
+    too many for the parameter bank) run the streamed-record evaluator and the
+    G = 8 LU; 24 seeded total-degree paths must match the CPU oracle: same
+    statuses, endpoints within 1e-8."""
+    p = configs.total_degree_problem(f"Q{n}", configs.dense_quadrics(n, 100 + n), 100 + n)
+    idx = np.sort(np.random.default_rng(n).choice(2 ** n, 24, replace=False))
+    starts = np.concatenate([systems.total_degree_starts(p.degrees, int(i), 1) for i in idx])
+    res = tracker.track_batch(gpu_h(p), starts)
+    h = O.LinearHomotopy(p.start, p.target, p.gamma)
+    for i in range(len(idx)):
+        r = O.track(h, starts[i])
+        assert (res.status[i] in (0, 2)) == r.succeeded, (i, res.status[i], r.status)
+        if r.succeeded:
+            x = r.endpoint.coordinates
+            assert np.max(np.abs(res.x[i] - x)) / max(1.0, np.max(np.abs(x))) < 1e-8
