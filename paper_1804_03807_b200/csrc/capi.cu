@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -51,6 +52,12 @@ struct NidHomotopy {
   TermRec* rec = nullptr;  // streamed records (csrc/track_rec.cuh), n > 10
   uint4* runs = nullptr;
   int grun[17] = {0};
+  TermRec* srec = nullptr;  // shared-monomial tables (csrc/track_sme.cuh)
+  unsigned long long* smono = nullptr;
+  uint4* schunk = nullptr;
+  unsigned* scnt = nullptr;
+  int snchunk = 0;
+  int sbase[17] = {0};
   cudaLibrary_t jit_lib = nullptr;  // NVRTC-specialised tracker (nid_homotopy_jit)
   cudaKernel_t jit_kernel = nullptr;
   HomDev dev() const {
@@ -77,6 +84,12 @@ struct NidHomotopy {
     h.rec = rec;
     h.runs = runs;
     for (int v = 0; v <= 16; ++v) h.grun[v] = grun[v];
+    h.srec = srec;
+    h.smono = smono;
+    h.schunk = schunk;
+    h.scnt = scnt;
+    h.snchunk = snchunk;
+    for (int v = 0; v <= 16; ++v) h.sbase[v] = sbase[v];
     return h;
   }
 };
@@ -438,6 +451,128 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
         h->runs = nullptr;
       }
     }
+    // shared-monomial tables (csrc/track_sme.cuh): when the rows share their
+    // monomials (C3/C4: the eight heavy rows have the same 495-monomial
+    // support), each distinct monomial and its partials are formed once per
+    // slot and every row accumulates coefficient x (value, partials).
+    // Opt-in (NID_SME=1): measured slower than the streamed records on C3
+    // (1,475 vs 1,086 ms on the 18,944-path probe).
+    if (!e && h->rec && getenv("NID_SME") && atoi(getenv("NID_SME")) != 0) {
+      const int G = rows::groups_for(n);
+      std::map<std::vector<unsigned char>, int> mid;
+      std::vector<std::vector<unsigned char>> mono;
+      std::vector<int> term_mono(T, -1);
+      bool ok = G == 8;
+      for (int gg = 0; gg < G; ++gg) ok = ok && h->goff[gg + 1] - h->goff[gg] <= 2;  // two rows per warp at most
+      for (int k = 0; k < T && ok; ++k) {
+        std::vector<unsigned char> ex(d->expo + k * NID_MAX_VARS, d->expo + k * NID_MAX_VARS + n);
+        int deg = 0;
+        for (int v = 0; v < n; ++v) deg += ex[v];
+        if (deg == 0) continue;
+        if (deg > SME_KM) ok = false;
+        auto it = mid.find(ex);
+        if (it == mid.end()) {
+          it = mid.emplace(ex, (int)mono.size()).first;
+          mono.push_back(ex);
+        }
+        term_mono[k] = it->second;
+      }
+      const int pairs = T;  // (row, term) pairs
+      ok = ok && !mono.empty() && pairs >= 2 * (int)mono.size();
+      if (ok) {
+        // monomials by degree, chunks of up to G per degree
+        std::vector<int> order(mono.size());
+        for (size_t z = 0; z < order.size(); ++z) order[z] = (int)z;
+        auto degof = [&](int m) {
+          int dd = 0;
+          for (int v = 0; v < n; ++v) dd += mono[m][v];
+          return dd;
+        };
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return degof(a) < degof(b); });
+        std::vector<int> pos_of(mono.size());
+        std::vector<uint4> chunks;
+        std::vector<unsigned long long> smono;
+        for (size_t z = 0; z < order.size();) {
+          const int K = degof(order[z]);
+          size_t z1 = z;
+          while (z1 < order.size() && degof(order[z1]) == K && (int)(z1 - z) < G) ++z1;
+          chunks.push_back(make_uint4((unsigned)K, (unsigned)smono.size(), (unsigned)(z1 - z), 0u));
+          for (size_t w = z; w < z1; ++w) {
+            const int m = order[w];
+            pos_of[m] = (int)smono.size();
+            unsigned long long meta = 0;
+            int np = 0;
+            for (int v = 0; v < n; ++v)
+              for (int a = 0; a < mono[m][v]; ++a) {
+                meta |= (unsigned long long)v << (4 * np);
+                if (a > 0) meta |= 1ull << (52 + np);
+                ++np;
+              }
+            meta |= (unsigned long long)np << 48;
+            smono.push_back(meta);
+          }
+          z = z1;
+        }
+        const int NC = (int)chunks.size();
+        // consumer records per warp group: chunk by chunk, the group's rows'
+        // terms whose monomial is in the chunk (constants with chunk 0)
+        std::vector<TermRec> srec;
+        std::vector<unsigned> scnt((size_t)NC * G, 0u);
+        for (int gg = 0; gg < G; ++gg) {
+          h->sbase[gg] = (int)srec.size();
+          for (int c = 0; c < NC; ++c) {
+            const unsigned lo = chunks[c].y, hi = chunks[c].y + chunks[c].z;
+            unsigned cnt = 0;
+            for (int gi = h->goff[gg], li = 0; gi < h->goff[gg + 1]; ++gi, ++li) {
+              const int i = h->grow[gi];
+              for (int k = off[i]; k < off[i + 1]; ++k) {
+                const int m = term_mono[k];
+                const bool cst = m < 0;
+                if (cst ? c != 0 : ((unsigned)pos_of[m] < lo || (unsigned)pos_of[m] >= hi)) continue;
+                TermRec r;
+                memset(&r, 0, sizeof(r));
+                r.ctr = d->coef_target[2 * k];
+                r.cti = d->coef_target[2 * k + 1];
+                r.csr = d->coef_start[2 * k];
+                r.csi = d->coef_start[2 * k + 1];
+                r.acs = acs[k];
+                r.act = act[k];
+                r.meta = cst ? 0ull : smono[pos_of[m]];
+                r.pslot = d->param_slot ? (int)d->param_slot[k] : -1;
+                r.pad = (cst ? 0x100 : (pos_of[m] - (int)lo)) | (li << 4);
+                srec.push_back(r);
+                ++cnt;
+              }
+            }
+            scnt[(size_t)c * G + gg] = cnt;
+          }
+        }
+        for (int gg = G; gg <= 16; ++gg) h->sbase[gg] = (int)srec.size();
+        for (int z = 0; z < 16; ++z) {  // the ring reads up to two chunks past a stream's end
+          TermRec r;
+          memset(&r, 0, sizeof(r));
+          srec.push_back(r);
+        }
+        h->snchunk = NC;
+        e = cudaMalloc(&h->srec, srec.size() * sizeof(TermRec));
+        if (!e) e = cudaMemcpy(h->srec, srec.data(), srec.size() * sizeof(TermRec), cudaMemcpyHostToDevice);
+        if (!e) e = cudaMalloc(&h->smono, smono.size() * sizeof(unsigned long long));
+        if (!e) e = cudaMemcpy(h->smono, smono.data(), smono.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice);
+        if (!e) e = cudaMalloc(&h->schunk, chunks.size() * sizeof(uint4));
+        if (!e) e = cudaMemcpy(h->schunk, chunks.data(), chunks.size() * sizeof(uint4), cudaMemcpyHostToDevice);
+        if (!e) e = cudaMalloc(&h->scnt, scnt.size() * sizeof(unsigned));
+        if (!e) e = cudaMemcpy(h->scnt, scnt.data(), scnt.size() * sizeof(unsigned), cudaMemcpyHostToDevice);
+        if (e) {
+          cudaFree(h->srec);
+          cudaFree(h->smono);
+          cudaFree(h->schunk);
+          cudaFree(h->scnt);
+          h->srec = nullptr;
+          h->snchunk = 0;
+          e = cudaSuccess;
+        }
+      }
+    }
   }
   if (!e && T) e = cudaMemcpy(h->cs, d->coef_start, T * sizeof(cd), cudaMemcpyHostToDevice);
   if (!e && T) e = cudaMemcpy(h->ct, d->coef_target, T * sizeof(cd), cudaMemcpyHostToDevice);
@@ -511,6 +646,10 @@ int nid_homotopy_destroy(NidHomotopy* h) {
   cudaFree(h->fex);
   if (h->rec) cudaFree(h->rec);
   if (h->runs) cudaFree(h->runs);
+  if (h->srec) cudaFree(h->srec);
+  if (h->smono) cudaFree(h->smono);
+  if (h->schunk) cudaFree(h->schunk);
+  if (h->scnt) cudaFree(h->scnt);
   cudaFree(h->cs);
   cudaFree(h->ct);
   cudaFree(h->acs);

@@ -30,6 +30,7 @@
 #include "track_ptab.cuh"
 #include "track_rec.cuh"
 #include "track_rows.cuh"
+#include "track_sme.cuh"
 
 namespace ctl {
 
@@ -208,7 +209,7 @@ constexpr size_t ring_bytes() {
 }
 template <int N>
 constexpr size_t smem_bytes() {
-  return Lay<N>::bytes() + ring_bytes<N>();
+  return Lay<N>::bytes() + ring_bytes<N>() + (N > 10 ? sme::bytes() : 0);
 }
 
 // blocks per SM the register budget is sized for: as many as the shared
@@ -216,7 +217,10 @@ constexpr size_t smem_bytes() {
 template <int N>
 constexpr int min_blocks() {
   constexpr int fit = (int)((228u * 1024u) / (smem_bytes<N>() + 1024u));
-  constexpr int cap = Lay<N>::G <= 4 ? 3 : 2;
+#ifndef NID_MAXBLK
+#define NID_MAXBLK 3
+#endif
+  constexpr int cap = Lay<N>::G <= 4 ? NID_MAXBLK : 2;
   return fit < 1 ? 1 : (fit > cap ? cap : fit);
 }
 
@@ -718,8 +722,13 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
         const long long pr = lb[S + lane];
         const cd* prm = (act && pr >= 0) ? Ar.params + pr : nullptr;
         TermRec* ring = reinterpret_cast<TermRec*>(smem_ctl + L::bytes()) + g * 2 * rec::CHUNK;
-        eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
-                         db + L::AXW * S + lane, ring);
+        if (Ar.H.srec) {  // shared monomials (every warp of the block takes part)
+          eval_rows_sme<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+                           db + L::AXW * S + lane, ring, smem_ctl + L::bytes() + ring_bytes<N>());
+        } else {
+          eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+                           db + L::AXW * S + lane, ring);
+        }
         rec_done = true;
       }
     }
