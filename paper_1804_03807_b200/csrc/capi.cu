@@ -342,7 +342,7 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
     // streamed records for the large-system tracker (csrc/track_rec.cuh): per
     // warp group, its rows in order, each row's terms grouped by factor count
     // (stable), records contiguous; every term of total degree <= 12
-    bool rec_ok = n > 10;
+    bool rec_ok = n >= 8 && !h->ptab;  // ctl::rec_on<n>()
     for (int k = 0; k < T && rec_ok; ++k) {
       int deg = 0;
       for (int v = 0; v < n; ++v) deg += d->expo[k * NID_MAX_VARS + v];

@@ -201,11 +201,18 @@ NID_D void lu_run(cd* augs, int q, bool solving, unsigned long long& perm, bool&
   if constexpr (MCK > 1) lu_run<N, G, CPW, MCK - 1>(augs, q, solving, perm, bad, pk);
 }
 
-// dynamic shared memory of the tracker: the slot layout, plus (n > 10) each
-// warp's ring of streamed term records (track_rec.cuh)
+// the table kernel streams term records (track_rec.cuh) for n >= 8 (tables
+// too large for the parameter bank: C3's cascade levels n = 8..14, C4)
+template <int N>
+constexpr bool rec_on() {
+  return N >= 8;
+}
+// dynamic shared memory of the table kernel: the slot layout, each warp's
+// ring of streamed term records, (n > 10) the shared-monomial exchange area;
+// the parameter-bank kernel needs the slot layout only
 template <int N>
 constexpr size_t ring_bytes() {
-  return N > 10 ? (size_t)rows::groups<N>() * 2 * rec::CHUNK * sizeof(TermRec) : 0;
+  return rec_on<N>() ? (size_t)rows::groups<N>() * 2 * rec::CHUNK * sizeof(TermRec) : 0;
 }
 template <int N>
 constexpr size_t smem_bytes() {
@@ -215,13 +222,18 @@ constexpr size_t smem_bytes() {
 // blocks per SM the register budget is sized for: as many as the shared
 // memory admits (228 KB per SM, 1 KB reserved per block), at most 3
 template <int N>
-constexpr int min_blocks() {
-  constexpr int fit = (int)((228u * 1024u) / (smem_bytes<N>() + 1024u));
-#ifndef NID_MAXBLK
-#define NID_MAXBLK 3
-#endif
-  constexpr int cap = Lay<N>::G <= 4 ? NID_MAXBLK : 2;
+constexpr int blocks_for_smem(size_t smem) {
+  const int fit = (int)((228u * 1024u) / (smem + 1024u));
+  const int cap = Lay<N>::G <= 4 ? 3 : 2;
   return fit < 1 ? 1 : (fit > cap ? cap : fit);
+}
+template <int N>
+constexpr int min_blocks() {  // table kernel
+  return blocks_for_smem<N>(smem_bytes<N>());
+}
+template <int N>
+constexpr int min_blocks_pt() {  // parameter-bank kernel
+  return blocks_for_smem<N>(Lay<N>::bytes());
 }
 
 }  // namespace ctl
@@ -715,17 +727,22 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     if (!__syncthreads_or(W_IS(I_ACT) != A_IDLE)) break;
     NID_TP(1);  // barrier before the evaluation
     bool rec_done = false;
-    if constexpr (N > 10 && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value) {
+    if constexpr (rec_on<N>() && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value) {
       if (Ar.H.rec) {  // streamed records: every lane of the warp takes part
         const bool act = W_IS(I_ACT) == A_EVAL;
         const bool want = act && (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
         const long long pr = lb[S + lane];
         const cd* prm = (act && pr >= 0) ? Ar.params + pr : nullptr;
         TermRec* ring = reinterpret_cast<TermRec*>(smem_ctl + L::bytes()) + g * 2 * rec::CHUNK;
-        if (Ar.H.srec) {  // shared monomials (every warp of the block takes part)
-          eval_rows_sme<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
-                           db + L::AXW * S + lane, ring, smem_ctl + L::bytes() + ring_bytes<N>());
-        } else {
+        bool sme_done = false;
+        if constexpr (N > 10) {
+          if (Ar.H.srec) {  // shared monomials (every warp of the block takes part)
+            eval_rows_sme<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+                             db + L::AXW * S + lane, ring, smem_ctl + L::bytes() + ring_bytes<N>());
+            sme_done = true;
+          }
+        }
+        if (!sme_done) {
           eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
                            db + L::AXW * S + lane, ring);
         }
@@ -894,7 +911,7 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>())
 }
 
 template <int N>
-__global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>())
+__global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks_pt<N>())
     track_pt_kernel(const __grid_constant__ TrackArgsPT A) {
   track_body<N, TableEval<N>, PTab>(A.a, &A.t);
 }
