@@ -282,7 +282,7 @@ def native_arm(args, prob):
             "e2e": e2e,
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "track_ctl_kernel<10, JitEval>" if args.jit else "track_pt_kernel<10>",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "track_ctl_kernel<10, JitEval>" if args.jit else "track_pt_kernel<10, false>",
                          "peak_source": peak_src,
                          "algorithmic_flop_per_launch": flop, "kernel_ms_per_launch": k_ms,
                          "endpoint_kernel_ms_per_launch": e_ms, "share_of_step": k_ms / (ms / args.steps),

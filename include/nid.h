@@ -11,6 +11,7 @@
  * package `nidpipe` (/root/reference/pkg/src/nidpipe):
  *
  *   nid_homotopy_create   LinearHomotopy(start, target, gamma)       tracker.py:57-106
+ *                         PolyhedralHomotopy(g, cell, supports)      polyhedral.py:730-791
  *   nid_eval_batch        LinearHomotopy.eval / .jac / .eval_scale    tracker.py:81-92
  *                         (+ _StackedEvaluator, polynomials.py:202-256,282-287)
  *   nid_newton_step_batch newton_step (zgesv, lstsq fallback)          linalg.py:35-51
@@ -85,6 +86,14 @@ typedef struct NidHomotopyDesc {
    * table then carries only the target system (coef_start all zero). */
   int32_t start_kind;
   const int32_t* start_degrees;
+  /* start_kind 2: a per-cell polyhedral homotopy (PolyhedralHomotopy,
+   * polyhedral.py:730-791).  H(x, t) = sum_k c_k t^{term_texp[k]} x^{a_k}
+   * with c_k = coef_target[k] (coef_start all zero, gamma unused); the
+   * Jacobian terms carry the weight of the term they differentiate and the
+   * noise scale is max_i sum_k |c_k| t^{w_k} |x|^{a_k}.  term_texp holds the
+   * rescaled exponents (0 on the cell's pairs).  Tracked only through the
+   * parameter-bank kernel (at most 256 terms); larger tables are refused. */
+  const double* term_texp;  /* [nterms], start_kind 2 only */
 } NidHomotopyDesc;
 
 typedef struct NidHomotopy NidHomotopy;

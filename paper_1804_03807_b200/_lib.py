@@ -50,7 +50,7 @@ class HomotopyDescC(C.Structure):
         ("n", C.c_int32), ("nterms", C.c_int32), ("row_off", C.c_void_p), ("expo", C.c_void_p),
         ("coef_start", C.c_void_p), ("coef_target", C.c_void_p), ("param_slot", C.c_void_p),
         ("nparam", C.c_int32), ("gamma_re", C.c_double), ("gamma_im", C.c_double),
-        ("start_kind", C.c_int32), ("start_degrees", C.c_void_p),
+        ("start_kind", C.c_int32), ("start_degrees", C.c_void_p), ("term_texp", C.c_void_p),
     ]
 
 

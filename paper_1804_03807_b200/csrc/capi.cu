@@ -3,6 +3,7 @@
 // sizes the persistent grids and dispatches to the per-size kernels.
 #include <nvrtc.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -48,6 +49,7 @@ struct NidHomotopy {
   cd *cs, *ct;
   double *acs, *act;
   int8_t* pslot;
+  double* tw = nullptr;  // polyhedral t-exponents (start_kind 2) or null
   PTab* ptab = nullptr;  // host copy of the parameter-bank table (null: table too large / per-path params)
   TermRec* rec = nullptr;  // streamed records (csrc/track_rec.cuh), n > 10
   uint4* runs = nullptr;
@@ -81,6 +83,7 @@ struct NidHomotopy {
     h.act = act;
     h.pslot = pslot;
     h.gamma = gamma;
+    h.tw = tw;
     h.rec = rec;
     h.runs = runs;
     for (int v = 0; v <= 16; ++v) h.grun[v] = grun[v];
@@ -207,7 +210,15 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
       if (a > maxdeg) maxdeg = a;
     }
   }
-  if (d->start_kind != 0 && d->start_kind != 1) FAIL("unknown start_kind");
+  if (d->start_kind < 0 || d->start_kind > 2) FAIL("unknown start_kind");
+  if (d->start_kind == 2) {  // per-cell polyhedral homotopy (polyhedral.py:730-791)
+    if (!d->term_texp) FAIL("polyhedral homotopy needs term_texp");
+    if (d->param_slot) FAIL("polyhedral homotopy takes no per-path coefficients");
+    for (int k = 0; k < T; ++k)
+      if (!(d->term_texp[k] >= 0.0) || !std::isfinite(d->term_texp[k])) FAIL("term_texp must be finite and >= 0");
+    for (int k = 0; k < 2 * T; ++k)
+      if (d->coef_start[k] != 0.0) FAIL("polyhedral homotopy: the term table must hold only the start system g");
+  }
   if (d->start_kind == 1) {
     if (!d->start_degrees) FAIL("total-degree start needs start_degrees");
     for (int v = 0; v < n; ++v)
@@ -271,6 +282,8 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   e = e ? e : cudaMalloc(&h->act, Tp * sizeof(double));
   h->pslot = nullptr;
   if (!e && d->param_slot) e = cudaMalloc(&h->pslot, Tp);
+  if (!e && d->start_kind == 2) e = cudaMalloc(&h->tw, Tp * sizeof(double));
+  if (!e && d->start_kind == 2 && T) e = cudaMemcpy(h->tw, d->term_texp, T * sizeof(double), cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(h->row_off, off.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice);
   if (!e && T) e = cudaMemcpy(h->expo, d->expo, T * sizeof(uint4), cudaMemcpyHostToDevice);
   if (!e && T) {
@@ -334,6 +347,10 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
         pt->act[k] = act[k];
         pt->acs[k] = acs[k];
       }
+      if (d->start_kind == 2) {
+        pt->poly = 1;
+        for (int k = 0; k < T; ++k) pt->tw[k] = d->term_texp[k];
+      }
       if (fits) h->ptab = pt;
       else delete pt;
     }
@@ -342,7 +359,7 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
     // streamed records for the large-system tracker (csrc/track_rec.cuh): per
     // warp group, its rows in order, each row's terms grouped by factor count
     // (stable), records contiguous; every term of total degree <= 12
-    bool rec_ok = n >= 8 && !h->ptab;  // ctl::rec_on<n>()
+    bool rec_ok = n >= 8 && !h->ptab && d->start_kind != 2;  // ctl::rec_on<n>()
     for (int k = 0; k < T && rec_ok; ++k) {
       int deg = 0;
       for (int v = 0; v < n; ++v) deg += d->expo[k * NID_MAX_VARS + v];
@@ -655,6 +672,7 @@ int nid_homotopy_destroy(NidHomotopy* h) {
   cudaFree(h->acs);
   cudaFree(h->act);
   if (h->pslot) cudaFree(h->pslot);
+  if (h->tw) cudaFree(h->tw);
   delete h;
   return 0;
 }
@@ -698,6 +716,10 @@ int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, co
   memset(&g_counters, 0, sizeof(g_counters));
   if (P == 0) return 0;
   if (!starts && !degrees) FAIL("need explicit starts or total-degree degrees");
+  if (h->tw && (!h->ptab || h->jit_kernel || getenv("NID_NO_PTAB")))
+    FAIL("polyhedral homotopy: only the parameter-bank tracker (<= 256 terms, <= 1536 variable occurrences) "
+         "evaluates t-weighted coefficients");
+  if (h->tw && !starts) FAIL("polyhedral homotopy: explicit (binomial) start points are required");
   if (h->nparam > 0 && !params) FAIL("homotopy has per-path parameters but none were given");
   if (param_div < 1) param_div = 1;
 

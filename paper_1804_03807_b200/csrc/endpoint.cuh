@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(128) eval_kernel(EvalArgs E) {
     E.Hout[p * N + g.lg] = hv;
 #pragma unroll
     for (int v = 0; v < N; ++v) E.Jout[(p * N + g.lg) * N + v] = J[v];
-    if (g.lg == 0) E.scale[p] = (1.0 - t) * mS + t * mT;
+    if (g.lg == 0) E.scale[p] = E.H.tw ? mT : (1.0 - t) * mS + t * mT;
   }
 }
 

@@ -53,6 +53,9 @@ struct HomDev {
   const double* act;      // |ct|
   const int8_t* pslot;    // per-path target coefficient slot or null
   cd gamma;
+  // per-cell polyhedral homotopy (start_kind 2): coefficient k is
+  // ct[k] * t^tw[k] (polyhedral.py:764-781); null for a linear homotopy
+  const double* tw;
   // streamed records (n > 10, every term of total degree <= 12) or null:
   // group g evaluates runs [grun[g], grun[g+1]) of `runs` = {row, factor
   // count, first record, records}, whose records are contiguous
@@ -129,7 +132,8 @@ NID_D void eval_row(const HomDev& H, int row, const cd (&x)[N], double t, const 
       int s = H.pslot[k];
       if (s >= 0) ct = prm[s];
     }
-    const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
+    const double tp = H.tw ? pow(t, __ldg(H.tw + k)) : 1.0;
+    const cd c = H.tw ? tp * ct : (H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct);
     cd P[N];
     cd p = cd{1.0, 0.0};
     if (ml) {
@@ -197,11 +201,14 @@ NID_D void eval_row(const HomDev& H, int row, const cd (&x)[N], double t, const 
       double m = 1.0;
 #pragma unroll
       for (int v = 0; v < N; ++v) m = __dmul_rn(m, rpow_small(ax[v], expo_at(w, v), maxdeg));
+      if (H.tw) m = __dmul_rn(m, pow(t, __ldg(H.tw + k)));
       if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
       sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), m));
     }
     // |G_i| terms sorted as the reference stores them: constant, then x_i^d
     if (H.td && row < H.n) sS = __dadd_rn(1.0, xa_td);
+    // polyhedral: one weighted system, scale = its own abs sum whatever t
+    if (H.tw) sS = sT;
   }
 }
 

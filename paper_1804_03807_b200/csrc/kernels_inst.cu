@@ -41,7 +41,9 @@ int CAT(launch_track_, NID_N)(const TrackArgs& a, int max_blocks, cudaStream_t s
 
 // the same tracker with the term table in the launch's parameter bank
 int CAT(launch_track_pt_, NID_N)(const TrackArgsPT& a, int max_blocks, cudaStream_t s) {
-  const void* fn = (const void*)track_pt_kernel<NID_N>;
+  // a per-cell polyhedral homotopy (t-weighted coefficients) runs its own
+  // instantiation: the linear-homotopy kernel carries none of its code
+  const void* fn = a.t.poly ? (const void*)track_pt_kernel<NID_N, true> : (const void*)track_pt_kernel<NID_N, false>;
   const int threads = 32 * rows::groups<NID_N>();
   const int smem = (int)ctl::Lay<NID_N>::bytes();
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -50,7 +52,10 @@ int CAT(launch_track_pt_, NID_N)(const TrackArgsPT& a, int max_blocks, cudaStrea
   if (need < blocks) blocks = (int)need;
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  track_pt_kernel<NID_N><<<blocks, threads, smem, s>>>(a);
+  if (a.t.poly)
+    track_pt_kernel<NID_N, true><<<blocks, threads, smem, s>>>(a);
+  else
+    track_pt_kernel<NID_N, false><<<blocks, threads, smem, s>>>(a);
   return blocks;
 }
 
@@ -87,7 +92,7 @@ int CAT(track_regs_, NID_N)() {
 
 int CAT(track_pt_regs_, NID_N)() {
   cudaFuncAttributes at;
-  if (cudaFuncGetAttributes(&at, (const void*)track_pt_kernel<NID_N>) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&at, (const void*)track_pt_kernel<NID_N, false>) != cudaSuccess) return -1;
   return at.numRegs;
 }
 

@@ -670,7 +670,7 @@ struct has_table_flag<E, decltype((void)E::kTable)> {
 // table in global memory, read through L1) and the parameter-table kernel
 // (track_pt_kernel: csrc/track_ptab.cuh, the table in the launch's constant
 // bank).  Tab = void selects Eval; Tab = PTab selects PTEval.
-template <int N, class Eval, class Tab>
+template <int N, class Eval, class Tab, bool PO = false>
 __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) {
   using namespace ctl;
   using L = Lay<N>;
@@ -752,7 +752,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     if (!rec_done && W_IS(I_ACT) == A_EVAL) {
       const bool want = (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
       if constexpr (ctl::is_ptab<Tab>::value) {
-        PTEval<N>::rows(Ar.H, *tab, g, W_DS(D_TE), aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);
+        PTEval<N, PO>::rows(Ar.H, *tab, g, W_DS(D_TE), aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);
       } else {
         cd x[N];
 #pragma unroll
@@ -767,7 +767,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     NID_TP(3);  // barrier after the evaluation
     if (is_ctl && C_IS(I_ACT) == A_EVAL) {
       double sc = 0.0;
-      const double r = rows::combine_resid<N>(augc, partc, C_DS(D_TE), sc);
+      const double r = rows::combine_resid<N>(augc, partc, C_DS(D_TE), sc, PO);
       if (C_IS(I_FLAGS) & F_FALLBACK) {
         // zgesv failed at this point: min-norm least squares (zgelsd) on the
         // re-evaluated augmented matrix
@@ -910,8 +910,8 @@ __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks<N>())
   track_body<N, Eval, void>(Ar, nullptr);
 }
 
-template <int N>
+template <int N, bool PO>  // PO: per-cell polyhedral homotopy (start_kind 2)
 __global__ void __launch_bounds__(rows::groups<N>() * 32, ctl::min_blocks_pt<N>())
     track_pt_kernel(const __grid_constant__ TrackArgsPT A) {
-  track_body<N, TableEval<N>, PTab>(A.a, &A.t);
+  track_body<N, TableEval<N>, PTab, PO>(A.a, &A.t);
 }

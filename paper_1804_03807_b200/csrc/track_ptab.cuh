@@ -33,6 +33,8 @@ struct PTab {
   double acs[PT_MAXT];                       // |cs|
   unsigned foff[PT_MAXF];                    // v * SLOTS * sizeof(cd): byte offset of variable v
   unsigned char fexp[PT_MAXF];               // its exponent
+  double tw[PT_MAXT];                        // polyhedral t-exponents (start_kind 2)
+  int poly;                                  // coefficient k is ct[k] * t^tw[k]
 };
 
 struct TrackArgsPT {
@@ -53,7 +55,7 @@ NID_D double atd(const double* base, unsigned off) {  // |x_v| scratch: stride S
 }
 
 // the terms of one run (factor count K) of a row
-template <int N, int K, bool ML>
+template <int N, int K, bool ML, bool PO>
 NID_D void run(const PTab& T, int r, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, cd* row,
                cd& hv, double& sS, double& sT) {
   const int k0 = T.run_k0[r], cnt = T.run_n[r], f0 = T.run_f0[r];
@@ -61,7 +63,8 @@ NID_D void run(const PTab& T, int r, const cd* xs, const double* axs, bool ws, b
   for (int j = 0; j < cnt; ++j) {
     const int k = k0 + j, fb = f0 + j * K;
     const cd ct = T.ct[k];
-    const cd c = td ? t * ct : alpha * T.cs[k] + t * ct;
+    const double tp = PO ? pow(t, T.tw[k]) : 1.0;  // polyhedral.py:764-781
+    const cd c = PO ? tp * ct : (td ? t * ct : alpha * T.cs[k] + t * ct);
     // x (and the powers) stay in registers between the two passes for
     // narrow terms; wide terms re-read x in the suffix pass (register budget)
     constexpr bool KEEPX = K <= 6;
@@ -128,19 +131,20 @@ NID_D void run(const PTab& T, int r, const cd* xs, const double* axs, bool ws, b
 #pragma unroll
     for (int q = 0; q < K; ++q) at(row, off[q]) = Jv[q];
     if (ws) {
+      if (PO) m = __dmul_rn(m, tp);
       if (!td) sS = __dadd_rn(sS, __dmul_rn(T.acs[k], m));
       sT = __dadd_rn(sT, __dmul_rn(T.act[k], m));
     }
   }
 }
 
-template <int N, bool ML>
+template <int N, bool ML, bool PO>
 NID_D void dispatch(const PTab& T, int r, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t,
                     cd* row, cd& hv, double& sS, double& sT) {
   switch (T.run_K[r]) {
 #define NID_PT(KK)                                                                                   \
   case KK:                                                                                           \
-    if (KK <= N) run<N, (KK <= N ? KK : 1), ML>(T, r, xs, axs, ws, td, alpha, t, row, hv, sS, sT); \
+    if (KK <= N) run<N, (KK <= N ? KK : 1), ML, PO>(T, r, xs, axs, ws, td, alpha, t, row, hv, sS, sT); \
     return;
     NID_PT(1) NID_PT(2) NID_PT(3) NID_PT(4) NID_PT(5) NID_PT(6) NID_PT(7) NID_PT(8)
     NID_PT(9) NID_PT(10) NID_PT(11) NID_PT(12) NID_PT(13) NID_PT(14) NID_PT(15) NID_PT(16)
@@ -153,18 +157,20 @@ NID_D void dispatch(const PTab& T, int r, const cd* xs, const double* axs, bool 
 #pragma unroll 1
   for (int k = k0; k < k0 + cnt; ++k) {
     const cd ct = T.ct[k];
-    hv = hv + (td ? t * ct : alpha * T.cs[k] + t * ct);
+    const double tp = PO ? pow(t, T.tw[k]) : 1.0;
+    hv = hv + (PO ? tp * ct : (td ? t * ct : alpha * T.cs[k] + t * ct));
     if (ws) {
-      if (!td) sS = __dadd_rn(sS, T.acs[k]);
-      sT = __dadd_rn(sT, T.act[k]);
+      if (!td) sS = __dadd_rn(sS, PO ? __dmul_rn(T.acs[k], tp) : T.acs[k]);
+      sT = __dadd_rn(sT, PO ? __dmul_rn(T.act[k], tp) : T.act[k]);
     }
   }
 }
 
 }  // namespace ptab
 
-// evaluator policy of track_pt_kernel (same contract as TableEval::rows)
-template <int N>
+// evaluator policy of track_pt_kernel (same contract as TableEval::rows);
+// PO: coefficients weighted by t^tw (per-cell polyhedral homotopy)
+template <int N, bool PO = false>
 struct PTEval {
   static NID_D void rows(const HomDev& H, const PTab& T, int g, double t, cd* aug, double* dbl, bool want_scale,
                          const cd* xs, double* axw) {
@@ -191,10 +197,12 @@ struct PTEval {
       double sS = 0.0, sT = 0.0;
 #pragma unroll 1
       for (int r = T.row_run[i]; r < T.row_run[i + 1]; ++r) {
-        if (H.multilinear)
-          ptab::dispatch<N, true>(T, r, xs, axw, ws, td, alpha, t, row, hv, sS, sT);
+        if constexpr (PO)  // per-cell polyhedral homotopy (start_kind 2)
+          ptab::dispatch<N, false, true>(T, r, xs, axw, ws, td, alpha, t, row, hv, sS, sT);
+        else if (H.multilinear)
+          ptab::dispatch<N, true, false>(T, r, xs, axw, ws, td, alpha, t, row, hv, sS, sT);
         else
-          ptab::dispatch<N, false>(T, r, xs, axw, ws, td, alpha, t, row, hv, sS, sT);
+          ptab::dispatch<N, false, false>(T, r, xs, axw, ws, td, alpha, t, row, hv, sS, sT);
       }
       if (td) {  // G_i = x_i^{d_i} - 1 in closed form
         const int d = H.tddeg[i];

@@ -399,7 +399,7 @@ NID_D void eval_rows_fac(const HomDev& H, int g, const cd* xs, double t, const c
 
 // combine the G partial maxima (after a barrier): residual max|H_i| and scale
 template <int N>
-NID_D double combine_resid(const cd* aug, const double* dbl, double t, double& scale) {
+NID_D double combine_resid(const cd* aug, const double* dbl, double t, double& scale, bool poly = false) {
   using L = Layout<N>;
   double r2 = 0.0, mS = 0.0, mT = 0.0;
 #pragma unroll
@@ -408,7 +408,7 @@ NID_D double combine_resid(const cd* aug, const double* dbl, double t, double& s
     mS = fmax(mS, dbl[(L::SS + g) * SLOTS]);
     mT = fmax(mT, dbl[(L::ST + g) * SLOTS]);
   }
-  scale = (1.0 - t) * mS + t * mT;
+  scale = poly ? mT : (1.0 - t) * mS + t * mT;  // polyhedral: one weighted system
   if (r2 < 1e290) return sqrt(r2);  // NaN takes the exact path as well
   double resid = 0.0;
 #pragma unroll 1

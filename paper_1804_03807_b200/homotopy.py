@@ -67,6 +67,7 @@ class Lowered:
     nparam: int
     gamma: complex
     start_degrees: np.ndarray | None = None  # int32 [n] when the start is total degree
+    texp: np.ndarray | None = None  # float64 [T]: per-cell polyhedral t-exponents (start_kind 2)
 
     @property
     def nterms(self) -> int:
@@ -143,11 +144,12 @@ class DeviceHomotopy:
     def __init__(self, low: Lowered):
         L = _lib.lib()
         self.low = low
-        self._keep = (low.row_off, low.expo, low.cs, low.ct, low.pslot, low.start_degrees)
+        self._keep = (low.row_off, low.expo, low.cs, low.ct, low.pslot, low.start_degrees, low.texp)
+        kind = 2 if low.texp is not None else (0 if low.start_degrees is None else 1)
         d = _lib.HomotopyDescC(
             low.n, low.nterms, _lib.ptr(low.row_off), _lib.ptr(low.expo), _lib.ptr(low.cs), _lib.ptr(low.ct),
             _lib.ptr(low.pslot), low.nparam, low.gamma.real, low.gamma.imag,
-            0 if low.start_degrees is None else 1, _lib.ptr(low.start_degrees))
+            kind, _lib.ptr(low.start_degrees), _lib.ptr(low.texp))
         h = C.c_void_p()
         _lib.check(L.nid_homotopy_create(C.byref(d), C.byref(h)), L)
         self.handle = h

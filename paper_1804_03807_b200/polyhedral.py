@@ -1,0 +1,220 @@
+"""Per-cell polyhedral tracking on the GPU.
+
+Mirrors the reference's polyhedral start-system surface
+(`nidpipe/polyhedral.py`):
+
+  * `PolyhedralHomotopy(g, cell, supports)`  polyhedral.py:730-791 -- lowered
+    to a term table whose coefficient k is c_k t^{w_k} (start_kind 2 of the
+    C-ABI, `include/nid.h`), with w the cell's lifted slacks rescaled so the
+    smallest positive one is 1 (exponents <= SLACK_MARGIN become 0)
+  * `binomial_solutions(V, beta)`            polyhedral.py:696-727
+  * `solve_cell(cell, g, supports, params)`  polyhedral.py:794-811, one launch
+  * `solve_cells(cells, g, supports, params)` every cell of a mixed
+    subdivision, one launch per cell, results in cell order (what
+    `solve_start_system`'s consume loop collects, cascade.py:134-141)
+
+Mixed-cell enumeration (the CPU LP, polyhedral.py:597-621) stays on the host
+and is not part of this package: cells are the reference's `MixedCell`
+objects (duck-typed: `.pairs`, `.texps`, `.volume`) or `Cell` below.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .homotopy import DeviceHomotopy, Lowered, TrackParams, eval_batch
+
+SLACK_MARGIN = 1e-9  # polyhedral.py:30
+
+
+@dataclass(frozen=True)
+class Cell:
+    """A fine mixed cell (polyhedral.py:75-87): one edge (a, b) per support
+    and the t-exponent of every support point (0 on the chosen pairs)."""
+
+    pairs: tuple
+    texps: tuple
+    volume: int = 0
+    normal: tuple = ()
+
+
+def supports_of(f) -> tuple:
+    """Sorted, deduplicated exponent sets per polynomial (polyhedral.py:45-52)."""
+    out = []
+    for i, p in enumerate(f.polys):
+        if not p.terms:
+            raise ValueError(f"polynomial {i} is zero; it has no Newton polytope")
+        out.append(tuple(sorted({tuple(int(v) for v in e) for e, _ in p.terms})))
+    return tuple(out)
+
+
+def rescaled_texps(cell) -> np.ndarray:
+    """The cell's t-exponents, row after row, divided by the smallest one
+    above SLACK_MARGIN; the others become 0 (polyhedral.py:784-789)."""
+    raw = np.concatenate([np.asarray(t, dtype=np.float64) for t in cell.texps]) if cell.texps else np.zeros(0)
+    pos = raw[raw > SLACK_MARGIN]
+    scale = 1.0 / pos.min() if pos.size else 1.0
+    return np.where(raw > SLACK_MARGIN, raw * scale, 0.0)
+
+
+def lower_polyhedral(g, cell, supports) -> Lowered:
+    """Term table of the cell's homotopy: row i = g's row i in support order
+    (the reference pairs supports[i] with g.polys[i].terms positionally)."""
+    n = g.nvars
+    if len(g.polys) != n:
+        raise ValueError("the GPU tracker needs a square system (rows == variables)")
+    if n > _lib.MAX_VARS:
+        raise ValueError(f"at most {_lib.MAX_VARS} variables are supported")
+    offs, ex, ct = [0], [], []
+    for i, p in enumerate(g.polys):
+        pts = supports[i]
+        if len(p.terms) != len(pts):
+            raise ValueError("start system terms must align with the support")
+        if len(cell.texps[i]) != len(pts):
+            raise ValueError("the cell needs one t-exponent per support point")
+        for e, (_, c) in zip(pts, p.terms):
+            ex.append(tuple(int(v) for v in e))
+            ct.append(complex(c))
+        offs.append(len(ct))
+    T = len(ct)
+    expo = np.zeros((T, _lib.MAX_VARS), dtype=np.uint8)
+    if T:
+        arr = np.array(ex, dtype=np.int64).reshape(T, n)
+        if arr.min(initial=0) < 0 or arr.max(initial=0) > 255:
+            raise ValueError("exponents must lie in 0..255")
+        expo[:, :n] = arr
+    return Lowered(n, np.array(offs, dtype=np.int32), expo, np.zeros(T, np.complex128),
+                   np.array(ct, dtype=np.complex128), None, 0, 1.0 + 0j, None,
+                   np.ascontiguousarray(rescaled_texps(cell)))
+
+
+@dataclass(frozen=True)
+class PolyhedralHomotopy:
+    """Per-cell continuation (polyhedral.py:730-791): at t = 0 only the
+    cell's binomial system survives, at t = 1 the homotopy is g itself."""
+
+    g: object
+    cell: object
+    supports: tuple
+    _cache: dict = field(default_factory=dict, repr=False, compare=False)
+
+    @property
+    def dim(self) -> int:
+        return self.g.nvars
+
+    def lowered(self) -> Lowered:
+        low = self._cache.get("low")
+        if low is None:
+            low = lower_polyhedral(self.g, self.cell, self.supports)
+            self._cache["low"] = low
+        return low
+
+    def device(self) -> DeviceHomotopy:
+        dev = self._cache.get("dev")
+        if dev is None:
+            dev = DeviceHomotopy(self.lowered())
+            self._cache["dev"] = dev
+        return dev
+
+    def evaluate(self, X, T):
+        return eval_batch(self.device(), X, T)
+
+    def eval(self, x, t):
+        return self.evaluate(np.asarray(x)[None], np.array([t]))[0][0]
+
+    def jac(self, x, t):
+        return self.evaluate(np.asarray(x)[None], np.array([t]))[1][0]
+
+    def eval_scale(self, x, t):
+        return float(self.evaluate(np.asarray(x)[None], np.array([t]))[2][0])
+
+
+def _hermite_lower(V):
+    """(L, U): U unimodular, L = V U lower triangular with a positive
+    diagonal.  Column Euclid row by row; exact integer arithmetic."""
+    n = len(V)
+    M = np.array(V, dtype=object).reshape(n, n)
+    U = np.eye(n, dtype=np.int64).astype(object)
+    for k in range(n):
+        while True:
+            cols = [j for j in range(k, n) if M[k, j] != 0]
+            if not cols:
+                raise ValueError("the cell's edge matrix is singular")
+            p = min(cols, key=lambda j: abs(M[k, j]))
+            if p != k:
+                M[:, [k, p]] = M[:, [p, k]]
+                U[:, [k, p]] = U[:, [p, k]]
+            rest = [j for j in range(k + 1, n) if M[k, j] != 0]
+            if not rest:
+                break
+            for j in rest:
+                q = M[k, j] // M[k, k]
+                M[:, j] -= q * M[:, k]
+                U[:, j] -= q * U[:, k]
+        if M[k, k] < 0:
+            M[:, k] = -M[:, k]
+            U[:, k] = -U[:, k]
+    return M, U
+
+
+def binomial_solutions(V, beta) -> np.ndarray:
+    """All solutions of y^(rows of V) = beta in the complex torus
+    (polyhedral.py:696-727): with L = V U lower triangular, solve w^L = beta
+    level by level (L[k][k] roots per level, every branch at once), then
+    y_l = prod_j w_j^{U[l][j]}.  Returns [|det V|, n] complex128."""
+    n = len(V)
+    L, U = _hermite_lower(V)
+    beta = np.asarray(beta, dtype=np.complex128)
+    W = np.ones((1, 0), dtype=np.complex128)
+    for k in range(n):
+        rhs = np.full(W.shape[0], beta[k])
+        for j in range(k):
+            rhs = rhs / W[:, j] ** int(L[k, j])
+        m = int(L[k, k])
+        r = np.abs(rhs) ** (1.0 / m)
+        th = np.angle(rhs)
+        ls = np.arange(m)
+        wk = r[:, None] * np.exp(1j * (th[:, None] + 2.0 * np.pi * ls[None, :]) / m)
+        W = np.concatenate([np.repeat(W, m, axis=0), wk.reshape(-1, 1)], axis=1)
+    Y = np.ones((W.shape[0], n), dtype=np.complex128)
+    for l in range(n):
+        for j in range(n):
+            e = int(U[l, j])
+            if e:
+                Y[:, l] *= W[:, j] ** e
+    return Y
+
+
+def cell_starts(cell, g) -> np.ndarray:
+    """The cell's binomial start system and its roots (polyhedral.py:800-808)."""
+    n = g.nvars
+    coeff_of = [dict((tuple(int(v) for v in e), complex(c)) for e, c in p.terms) for p in g.polys]
+    V, beta = [], []
+    for i, (a, b) in enumerate(cell.pairs):
+        a, b = tuple(int(v) for v in a), tuple(int(v) for v in b)
+        V.append([b[j] - a[j] for j in range(n)])
+        beta.append(-coeff_of[i][a] / coeff_of[i][b])
+    return binomial_solutions(V, beta)
+
+
+def solve_cell(cell, g, supports, params: TrackParams = TrackParams(), mode: str = "gpu"):
+    """Track the cell's volume-many paths from its binomial system to g at
+    t = 1 (polyhedral.py:794-811) in one launch; list[PathResult]."""
+    if mode != "gpu":
+        raise ValueError(f"unknown mode {mode!r}: this package tracks on the GPU")
+    from .tracker import track_batch
+
+    starts = cell_starts(cell, g)
+    h = PolyhedralHomotopy(g, cell, tuple(supports))
+    return track_batch(h, starts, params).path_results()
+
+
+def solve_cells(cells, g, supports, params: TrackParams = TrackParams(), mode: str = "gpu"):
+    """Every cell in order, results concatenated (cascade.py:134-141)."""
+    out = []
+    for cell in cells:
+        out.extend(solve_cell(cell, g, supports, params, mode))
+    return out

@@ -105,7 +105,7 @@ class TrackResults:
 def _device_of(h) -> DeviceHomotopy:
     if isinstance(h, DeviceHomotopy):
         return h
-    if isinstance(h, LinearHomotopy):
+    if isinstance(h, LinearHomotopy) or (hasattr(h, "lowered") and hasattr(h, "device")):  # + PolyhedralHomotopy
         return h.device()
     if all(hasattr(h, a) for a in ("start", "target", "gamma")):
         # a reference nidpipe.tracker.LinearHomotopy (duck-typed: only
@@ -115,7 +115,7 @@ def _device_of(h) -> DeviceHomotopy:
             cache = (h, LinearHomotopy(h.start, h.target, complex(h.gamma)))
             _FOREIGN[id(h)] = cache
         return cache[1].device()
-    raise TypeError("expected a LinearHomotopy (the GPU path tracks lowered linear homotopies)")
+    raise TypeError("expected a LinearHomotopy or PolyhedralHomotopy (the GPU path tracks lowered homotopies)")
 
 
 _FOREIGN: dict = {}

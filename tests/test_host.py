@@ -132,7 +132,8 @@ def test_no_gpu_means_loud_failure():
 
 def test_ctypes_struct_layout_matches_header():
     assert ctypes.sizeof(_lib.TrackParamsC) == 4 * 8 + 2 * 4 + 4 * 8 + 2 * 4 + 8 + 2 * 4
-    assert ctypes.sizeof(_lib.HomotopyDescC) == 4 + 4 + 5 * 8 + 8 + 16 + 8 + 8  # ..., start_kind(+pad), degrees
+    # ..., start_kind(+pad), degrees, term_texp
+    assert ctypes.sizeof(_lib.HomotopyDescC) == 4 + 4 + 5 * 8 + 8 + 16 + 8 + 8 + 8
 
 
 @pytest.mark.parametrize("total,world", [(3628800, 8), (5040, 3), (7, 4), (0, 2)])

@@ -1,0 +1,160 @@
+"""Per-cell polyhedral tracking: the reference's
+`solve_cell` (polyhedral.py:794-811) on every fine mixed cell of the C1 and
+C2 supports, pinned by tests/golden/polyhedral_{c1,c2}.npz (made by running
+the reference, tests/golden/make_polyhedral.py).
+
+CPU tests pin the oracle restatement (oracle/polyhedral.py) and the host-side
+binomial start solver against the reference's outputs; GPU tests compare the
+CUDA tracker (start_kind 2 of the C-ABI) with the same fixtures.  Bar:
+statuses and finite counts exact per cell, endpoints matched as sets within
+1e-8 relative, evaluation within 1e-13 of the oracle.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import nid_oracle as O
+from oracle import polyhedral as OP
+from paper_1804_03807_b200 import polyhedral as PH
+from paper_1804_03807_b200.polys import PolySystem, make_poly
+
+STATUS = {"converged": 0, "at_infinity": 1, "singular_endpoint": 2, "failed": 3}
+
+
+def load(name):
+    g = golden(f"polyhedral_{name}")
+    n = int(g["n"])
+    off = g["row_off"]
+    sup = g["support"]
+    supports = tuple(tuple(tuple(int(v) for v in sup[k]) for k in range(off[i], off[i + 1])) for i in range(n))
+    polys = tuple(make_poly(n, [(supports[i][j], g["coef"][off[i] + j]) for j in range(off[i + 1] - off[i])])
+                  for i in range(n))
+    gs = PolySystem(n, polys)
+    cells = []
+    for c in range(int(g["ncells"])):
+        pr = g[f"c{c}_pairs"]
+        tx = g[f"c{c}_texps"]
+        cells.append(PH.Cell(tuple((tuple(map(int, pr[i, 0])), tuple(map(int, pr[i, 1]))) for i in range(n)),
+                             tuple(tuple(tx[off[i]:off[i + 1]]) for i in range(n)), int(g[f"c{c}_volume"])))
+    return g, gs, supports, cells
+
+
+def match_sets(A, B, rel=1e-8):
+    """Every row of A has a distinct partner in B within rel * max(1, |b|)."""
+    A, B = np.asarray(A), np.asarray(B)
+    assert len(A) == len(B)
+    used = np.zeros(len(B), bool)
+    for a in A:
+        d = np.max(np.abs(B - a[None]), axis=1)
+        d[used] = np.inf
+        j = int(np.argmin(d))
+        assert d[j] <= rel * max(1.0, np.max(np.abs(B[j]))), (a, B[j], d[j])
+        used[j] = True
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_mixed_volume_and_cells(name):
+    g, gs, supports, cells = load(name)
+    assert sum(c.volume for c in cells) == {"c1": 16, "c2": 924}[name]
+    assert PH.supports_of(gs) == supports
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_binomial_starts_match_reference(name):
+    """Host solver and oracle against the reference's binomial_solutions."""
+    g, gs, supports, cells = load(name)
+    for c, cell in enumerate(cells):
+        ref = g[f"c{c}_starts"]
+        host = PH.cell_starts(cell, gs)
+        assert host.shape == ref.shape == (cell.volume, gs.nvars)
+        match_sets(host, ref, 1e-12)
+        match_sets(np.array(OP.cell_starts(gs, cell.pairs)), ref, 1e-12)
+
+
+def test_binomial_solutions_solve_the_system():
+    V = [[3, 1, 0], [-2, 2, 1], [0, -1, 4]]
+    beta = [0.3 + 1.1j, -2.0 + 0.5j, 0.7 - 0.2j]
+    Y = PH.binomial_solutions(V, beta)
+    assert len(Y) == abs(round(np.linalg.det(np.array(V, float))))
+    for y in Y:
+        for i in range(3):
+            assert abs(np.prod(y ** np.array(V[i])) - beta[i]) <= 1e-12 * abs(beta[i])
+    match_sets(Y, np.array(OP.binomial_solutions(V, beta)), 1e-12)
+
+
+def test_rescaled_texps_and_lowering():
+    g, gs, supports, cells = load("c2")
+    cell = cells[0]
+    w = PH.rescaled_texps(cell)
+    raw = np.concatenate([np.asarray(t) for t in cell.texps])
+    assert np.all(w[raw <= PH.SLACK_MARGIN] == 0.0)
+    assert np.isclose(w[raw > PH.SLACK_MARGIN].min(), 1.0)
+    np.testing.assert_array_equal(w, OP.rescale_texps(raw))
+    low = PH.lower_polyhedral(gs, cell, supports)
+    assert low.nterms == sum(len(s) for s in supports) and low.texp.shape == (low.nterms,)
+    assert not np.any(low.cs) and low.start_degrees is None
+    bad = PH.Cell(cell.pairs, (cell.texps[0][:-1],) + cell.texps[1:])
+    with pytest.raises(ValueError):
+        PH.lower_polyhedral(gs, bad, supports)
+
+
+def test_oracle_solve_cell_matches_reference_c1():
+    """Pins the oracle: its per-cell tracking reproduces the reference."""
+    g, gs, supports, cells = load("c1")
+    for c, cell in enumerate(cells):
+        res = OP.solve_cell(gs, cell.pairs, np.concatenate([np.asarray(t) for t in cell.texps]), supports)
+        st = np.array([STATUS[r.status] for r in res])
+        assert np.array_equal(np.sort(st), np.sort(g[f"c{c}_status"]))
+        ok = g[f"c{c}_status"] == 0
+        match_sets(np.array([r.endpoint.coordinates for r in res if r.status == "converged"]), g[f"c{c}_x"][ok])
+
+
+# ------------------------------------------------------------------ GPU
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_gpu_polyhedral_eval_matches_oracle(nid, name):
+    g, gs, supports, cells = load(name)
+    gen = np.random.default_rng(5)
+    for cell in cells[:6]:
+        h = PH.PolyhedralHomotopy(gs, cell, supports)
+        ho = OP.PolyhedralHomotopy(gs, np.concatenate([np.asarray(t) for t in cell.texps]), supports)
+        X = gen.normal(size=(5, gs.nvars)) + 1j * gen.normal(size=(5, gs.nvars))
+        T = np.array([0.0, 0.01, 0.37, 0.9, 1.0])
+        H, J, S = h.evaluate(X, T)
+        for i in range(5):
+            s = ho.eval_scale(X[i], T[i])
+            assert abs(S[i] - s) <= 1e-13 * max(1.0, s)
+            assert np.max(np.abs(H[i] - ho.eval(X[i], T[i]))) <= 1e-13 * max(1.0, s)
+            Jo = ho.jac(X[i], T[i])
+            assert np.max(np.abs(J[i] - Jo)) <= 1e-13 * max(1.0, np.max(np.abs(Jo)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_gpu_solve_cell_matches_reference(nid, name):
+    g, gs, supports, cells = load(name)
+    total = 0
+    for c, cell in enumerate(cells):
+        res = PH.solve_cell(cell, gs, supports)
+        assert len(res) == cell.volume
+        st = np.array([STATUS[r.status] for r in res])
+        assert np.array_equal(np.sort(st), np.sort(g[f"c{c}_status"])), c
+        ok = g[f"c{c}_status"] == 0
+        X = np.array([r.endpoint.coordinates for r in res if r.status == "converged"]).reshape(-1, gs.nvars)
+        match_sets(X, g[f"c{c}_x"][ok])
+        total += int(ok.sum())
+    assert total == {"c1": 16, "c2": 924}[name]
+
+
+@pytest.mark.gpu
+def test_gpu_solve_cells_roots_solve_g(nid):
+    """All 924 start-system roots of C2 from one call; each solves g."""
+    g, gs, supports, cells = load("c2")
+    res = PH.solve_cells(cells, gs, supports)
+    X = np.array([r.endpoint.coordinates for r in res if r.succeeded])
+    assert len(X) == 924
+    for x in X[::37]:
+        assert np.max(np.abs(O.eval_system(gs, x))) <= 1e-8
