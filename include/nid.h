@@ -21,6 +21,8 @@
  *                         _endpoint_solution / _dd_polish              tracker.py:255-302
  *   nid_track_batch_strided  the same over a rank's strided share of the
  *                         start-path indices (one process per GPU)     parallel.py:69-109
+ *   nid_track_cells       solve_start_system's per-cell solve_cell loop cascade.py:134-141,
+ *                         (cells batched, one t-exponent row per path) polyhedral.py:794-811
  *   nid_refine_batch      newton_refine + classify                     tracker.py:410-455
  *   nid_dd_refine_batch   refine_dd                                    tracker.py:431-435
  *   nid_match_pairs       points_match over all pairs (for _dedup)     filtering.py:73-78,140-150
@@ -157,6 +159,14 @@ int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, co
                             void* stream);
 
 int nid_last_counters(NidCounters* c);
+
+/* Many mixed cells of one polyhedral homotopy (start_kind 2) in one launch:
+ * path p starts at starts[p] and uses the t-exponent row
+ * path_texp[p * nterms .. (p+1) * nterms) instead of the handle's term_texp.
+ * Replaces the per-cell loop of solve_start_system (cascade.py:134-141) over
+ * solve_cell (polyhedral.py:794-811).  Outputs as nid_track_batch. */
+int nid_track_cells(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
+                    const double* path_texp, NidPathOut* out, int device_io, void* stream);
 
 /* Compile a homotopy-specialised tracker with NVRTC and attach it to h:
  * `src` is the evaluator source generated by paper_1804_03807_b200/jit.py,

@@ -694,8 +694,12 @@ int nid_last_counters(NidCounters* c) {
 // slot map for the workspace cache
 enum {
   W_STARTS = 0, W_PARAMS, W_XEND, W_STATUS, W_STEPS, W_TREACH, W_RESID, W_COND, W_REG,
-  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS, W_GSTATE
+  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS, W_GSTATE, W_PTW
 };
+
+static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, long long first_index,
+                      long long index_stride, const int32_t* degrees, const double* params, int param_div,
+                      const double* path_texp, NidPathOut* out, int device_io, void* stream);
 
 int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
                     long long first_index, const int32_t* degrees, const double* params, int param_div,
@@ -708,6 +712,20 @@ int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, co
                             long long first_index, long long index_stride, const int32_t* degrees,
                             const double* params, int param_div, NidPathOut* out, int device_io,
                             void* stream) {
+  return track_impl(h, prm, P, starts, first_index, index_stride, degrees, params, param_div, nullptr, out, device_io,
+                    stream);
+}
+
+int nid_track_cells(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, const double* path_texp,
+                    NidPathOut* out, int device_io, void* stream) {
+  if (!h || !h->tw) FAIL("nid_track_cells needs a polyhedral homotopy (start_kind 2)");
+  if (!starts || !path_texp) FAIL("nid_track_cells needs start points and per-path t-exponent rows");
+  return track_impl(h, prm, P, starts, 0, 1, nullptr, nullptr, 1, path_texp, out, device_io, stream);
+}
+
+static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, long long first_index,
+                      long long index_stride, const int32_t* degrees, const double* params, int param_div,
+                      const double* path_texp, NidPathOut* out, int device_io, void* stream) {
   if (!h || !prm || !out) FAIL("null argument");
   if (index_stride < 1) FAIL("index_stride must be >= 1");
   if (P < 0) FAIL("negative path count");
@@ -765,6 +783,17 @@ int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, co
     d_reg = ws<int8_t>(W_REG, P);
     if (!d_x || !d_st || !d_steps || !d_tr || !d_res || !d_cond || !d_reg) FAIL("out of device memory (outputs)");
   }
+  const double* d_ptw = nullptr;
+  if (path_texp) {
+    if (device_io) {
+      d_ptw = path_texp;
+    } else {
+      double* p = ws<double>(W_PTW, (size_t)P * (h->nterms > 0 ? h->nterms : 1));
+      if (!p) FAIL("out of device memory (t-exponent rows)");
+      CK(cudaMemcpyAsync(p, path_texp, (size_t)P * h->nterms * sizeof(double), cudaMemcpyHostToDevice, s));
+      d_ptw = p;
+    }
+  }
   unsigned long long* d_cnt = ws<unsigned long long>(W_COUNT, 16);
   if (!d_cnt) FAIL("out of device memory (counters)");
   CK(cudaMemsetAsync(d_cnt, 0, 16 * sizeof(unsigned long long), s));
@@ -798,6 +827,7 @@ int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, co
   }
   a.params = d_params;
   a.param_div = param_div;
+  a.ptw = d_ptw;
   a.next = d_cnt + 7;
   a.x_end = d_x;
   a.status = d_st;

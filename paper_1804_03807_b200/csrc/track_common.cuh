@@ -16,6 +16,7 @@ struct TrackArgs {
   const cd* roots;             // exp(2 pi i k / d_v), k < d_v
   const cd* params;       // per-path target coefficients
   int param_div;
+  const double* ptw;      // per-path polyhedral t-exponent rows [P][nterms] (cells batched) or null
   unsigned long long* next;  // claim counter
   cd* x_end;
   int8_t* status;

@@ -321,7 +321,7 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
         }
         const long long path = (long long)idx;
         lsl[0] = path;
-        lsl[S] = Ar.params ? (path / Ar.param_div) * Ar.H.nparam : -1;
+        lsl[S] = Ar.params ? (path / Ar.param_div) * Ar.H.nparam : (Ar.ptw ? path * Ar.H.nterms : -1);
         load_start<N>(Ar, path, xes);
         DS_(D_TE) = 0.0;
         IS_(I_USED) = 0;
@@ -752,7 +752,11 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     if (!rec_done && W_IS(I_ACT) == A_EVAL) {
       const bool want = (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
       if constexpr (ctl::is_ptab<Tab>::value) {
-        PTEval<N, PO>::rows(Ar.H, *tab, g, W_DS(D_TE), aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);
+        // batched cells: the slot's own t-exponent row (else the table's)
+        const double* tws = nullptr;
+        if constexpr (PO) tws = Ar.ptw ? Ar.ptw + lb[S + lane] : nullptr;
+        PTEval<N, PO>::rows(Ar.H, *tab, g, W_DS(D_TE), aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane,
+                            tws);
       } else {
         cd x[N];
 #pragma unroll

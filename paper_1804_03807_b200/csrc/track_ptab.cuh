@@ -57,13 +57,13 @@ NID_D double atd(const double* base, unsigned off) {  // |x_v| scratch: stride S
 // the terms of one run (factor count K) of a row
 template <int N, int K, bool ML, bool PO>
 NID_D void run(const PTab& T, int r, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, cd* row,
-               cd& hv, double& sS, double& sT) {
+               cd& hv, double& sS, double& sT, const double* tws) {
   const int k0 = T.run_k0[r], cnt = T.run_n[r], f0 = T.run_f0[r];
 #pragma unroll 1
   for (int j = 0; j < cnt; ++j) {
     const int k = k0 + j, fb = f0 + j * K;
     const cd ct = T.ct[k];
-    const double tp = PO ? pow(t, T.tw[k]) : 1.0;  // polyhedral.py:764-781
+    const double tp = PO ? pow(t, tws ? __ldg(tws + k) : T.tw[k]) : 1.0;  // polyhedral.py:764-781
     const cd c = PO ? tp * ct : (td ? t * ct : alpha * T.cs[k] + t * ct);
     // x (and the powers) stay in registers between the two passes for
     // narrow terms; wide terms re-read x in the suffix pass (register budget)
@@ -140,11 +140,11 @@ NID_D void run(const PTab& T, int r, const cd* xs, const double* axs, bool ws, b
 
 template <int N, bool ML, bool PO>
 NID_D void dispatch(const PTab& T, int r, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t,
-                    cd* row, cd& hv, double& sS, double& sT) {
+                    cd* row, cd& hv, double& sS, double& sT, const double* tws = nullptr) {
   switch (T.run_K[r]) {
 #define NID_PT(KK)                                                                                   \
   case KK:                                                                                           \
-    if (KK <= N) run<N, (KK <= N ? KK : 1), ML, PO>(T, r, xs, axs, ws, td, alpha, t, row, hv, sS, sT); \
+    if (KK <= N) run<N, (KK <= N ? KK : 1), ML, PO>(T, r, xs, axs, ws, td, alpha, t, row, hv, sS, sT, tws); \
     return;
     NID_PT(1) NID_PT(2) NID_PT(3) NID_PT(4) NID_PT(5) NID_PT(6) NID_PT(7) NID_PT(8)
     NID_PT(9) NID_PT(10) NID_PT(11) NID_PT(12) NID_PT(13) NID_PT(14) NID_PT(15) NID_PT(16)
@@ -157,7 +157,7 @@ NID_D void dispatch(const PTab& T, int r, const cd* xs, const double* axs, bool 
 #pragma unroll 1
   for (int k = k0; k < k0 + cnt; ++k) {
     const cd ct = T.ct[k];
-    const double tp = PO ? pow(t, T.tw[k]) : 1.0;
+    const double tp = PO ? pow(t, tws ? __ldg(tws + k) : T.tw[k]) : 1.0;
     hv = hv + (PO ? tp * ct : (td ? t * ct : alpha * T.cs[k] + t * ct));
     if (ws) {
       if (!td) sS = __dadd_rn(sS, PO ? __dmul_rn(T.acs[k], tp) : T.acs[k]);
@@ -173,7 +173,7 @@ NID_D void dispatch(const PTab& T, int r, const cd* xs, const double* axs, bool 
 template <int N, bool PO = false>
 struct PTEval {
   static NID_D void rows(const HomDev& H, const PTab& T, int g, double t, cd* aug, double* dbl, bool want_scale,
-                         const cd* xs, double* axw) {
+                         const cd* xs, double* axw, const double* tws = nullptr) {
     using L = rows::Layout<N>;
     constexpr int S = rows::SLOTS;
     const cd alpha = (1.0 - t) * H.gamma;
@@ -198,7 +198,7 @@ struct PTEval {
 #pragma unroll 1
       for (int r = T.row_run[i]; r < T.row_run[i + 1]; ++r) {
         if constexpr (PO)  // per-cell polyhedral homotopy (start_kind 2)
-          ptab::dispatch<N, false, true>(T, r, xs, axw, ws, td, alpha, t, row, hv, sS, sT);
+          ptab::dispatch<N, false, true>(T, r, xs, axw, ws, td, alpha, t, row, hv, sS, sT, tws);
         else if (H.multilinear)
           ptab::dispatch<N, true, false>(T, r, xs, axw, ws, td, alpha, t, row, hv, sS, sT);
         else

@@ -10,7 +10,8 @@ Mirrors the reference's polyhedral start-system surface
   * `binomial_solutions(V, beta)`            polyhedral.py:696-727
   * `solve_cell(cell, g, supports, params)`  polyhedral.py:794-811, one launch
   * `solve_cells(cells, g, supports, params)` every cell of a mixed
-    subdivision, one launch per cell, results in cell order (what
+    subdivision in ONE launch (`nid_track_cells`: each path carries its
+    cell's t-exponent row), results in cell order (what
     `solve_start_system`'s consume loop collects, cascade.py:134-141)
 
 Mixed-cell enumeration (the CPU LP, polyhedral.py:597-621) stays on the host
@@ -212,9 +213,49 @@ def solve_cell(cell, g, supports, params: TrackParams = TrackParams(), mode: str
     return track_batch(h, starts, params).path_results()
 
 
-def solve_cells(cells, g, supports, params: TrackParams = TrackParams(), mode: str = "gpu"):
-    """Every cell in order, results concatenated (cascade.py:134-141)."""
-    out = []
+def track_cells(cells, g, supports, params: TrackParams = TrackParams()):
+    """Every cell's paths in ONE launch (`nid_track_cells`): the starts of all
+    cells concatenated in cell order, each path carrying its cell's rescaled
+    t-exponent row.  Returns (TrackResults, per-cell path counts)."""
+    import ctypes as C
+
+    from .tracker import TrackResults
+
+    cells = list(cells)
+    if not cells:
+        raise ValueError("no cells")
+    supports = tuple(supports)
+    h = PolyhedralHomotopy(g, cells[0], supports)
+    dev = h.device()
+    n, T = g.nvars, h.lowered().nterms
+    starts, rows, counts = [], [], []
     for cell in cells:
-        out.extend(solve_cell(cell, g, supports, params, mode))
-    return out
+        st = cell_starts(cell, g)
+        w = rescaled_texps(cell)
+        if w.size != T:
+            raise ValueError("the cell needs one t-exponent per support point")
+        starts.append(st)
+        rows.append(np.broadcast_to(w, (len(st), T)))
+        counts.append(len(st))
+    st = np.ascontiguousarray(np.concatenate(starts), dtype=np.complex128)
+    tw = np.ascontiguousarray(np.concatenate(rows), dtype=np.float64)
+    P = st.shape[0]
+    out = TrackResults(np.empty((P, n), np.complex128), np.empty(P, np.int8), np.empty(P, np.int32),
+                       np.empty(P, np.float64), np.empty(P, np.float64), np.empty(P, np.float64),
+                       np.empty(P, np.int8), {})
+    o = _lib.PathOutC(_lib.ptr(out.x), _lib.ptr(out.status), _lib.ptr(out.steps), _lib.ptr(out.t_reached),
+                      _lib.ptr(out.residual), _lib.ptr(out.condition), _lib.ptr(out.regular))
+    L = _lib.lib()
+    pc = params.to_c()
+    _lib.check(L.nid_track_cells(dev.handle, C.byref(pc), P, _lib.ptr(st), _lib.ptr(tw), C.byref(o), 0, None), L)
+    out.counters = _lib.last_counters()
+    return out, counts
+
+
+def solve_cells(cells, g, supports, params: TrackParams = TrackParams(), mode: str = "gpu"):
+    """Every cell in order, results concatenated as solve_start_system's
+    consume loop collects them (cascade.py:134-141); one launch for all."""
+    if mode != "gpu":
+        raise ValueError(f"unknown mode {mode!r}: this package tracks on the GPU")
+    res, _ = track_cells(cells, g, supports, params)
+    return res.path_results()

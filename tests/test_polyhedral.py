@@ -150,11 +150,22 @@ def test_gpu_solve_cell_matches_reference(nid, name):
 
 
 @pytest.mark.gpu
-def test_gpu_solve_cells_roots_solve_g(nid):
-    """All 924 start-system roots of C2 from one call; each solves g."""
-    g, gs, supports, cells = load("c2")
-    res = PH.solve_cells(cells, gs, supports)
-    X = np.array([r.endpoint.coordinates for r in res if r.succeeded])
-    assert len(X) == 924
-    for x in X[::37]:
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_gpu_batched_cells_match_reference(nid, name):
+    """All cells in one launch (nid_track_cells): per-cell parity with the
+    reference, and every root solves g."""
+    g, gs, supports, cells = load(name)
+    res, counts = PH.track_cells(cells, gs, supports)
+    assert counts == [c.volume for c in cells]
+    pos = 0
+    for c, k in enumerate(counts):
+        st = res.status[pos:pos + k]
+        assert np.array_equal(np.sort(st), np.sort(g[f"c{c}_status"])), c
+        ok = g[f"c{c}_status"] == 0
+        match_sets(res.x[pos:pos + k][st == 0], g[f"c{c}_x"][ok])
+        pos += k
+    X = res.x[res.status == 0]
+    assert len(X) == {"c1": 16, "c2": 924}[name]
+    for x in X[::7]:
         assert np.max(np.abs(O.eval_system(gs, x))) <= 1e-8
+    assert len(PH.solve_cells(cells, gs, supports)) == sum(counts)
