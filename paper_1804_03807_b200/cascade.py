@@ -107,16 +107,30 @@ def top_homotopy(emb: EmbeddedSystem, seed: int | None = None) -> tuple[LinearHo
 
 
 def solve_top(emb: EmbeddedSystem, p: int = 1, seed: int | None = None, params: TrackParams = TrackParams(),
-              mode: str = "gpu", cell_log: list | None = None, return_arrays: bool = False):
-    """Continuation from the total-degree start to the embedded system
-    (cascade.py:214-246).  Returns (results, TopStats)."""
+              mode: str = "gpu", cell_log: list | None = None, return_arrays: bool = False, cells=None):
+    """Continuation onto the embedded system (cascade.py:214-246).  Returns
+    (results, TopStats).
+
+    Start system: the total-degree system by default.  With `cells` (the
+    fine mixed cells of the system's lifted supports, e.g. the reference's
+    `enumerate_cells(lift_supports(supports_of(system), seed, attempt))`,
+    which stays a host-side CPU LP) it is the reference's default polyhedral
+    start instead (solve_start_system, cascade.py:110-160): the random-
+    coefficient system g on the same supports, all cells tracked to g in one
+    launch (`polyhedral.track_cells`), then g -> system from g's roots."""
     _check_mode(mode)
+    if cells is not None:
+        return _solve_top_polyhedral(emb, seed, params, cells, cell_log, return_arrays)
     h, degrees = top_homotopy(emb, seed)
     total = int(np.prod(degrees, dtype=np.int64))
     stats = TopStats(start_paths=total)
     t0 = time.perf_counter()
     res = track_batch(h, None, params, degrees=degrees, count=total)
     stats.time_continuation = time.perf_counter() - t0
+    return _top_stats(res, stats, total, return_arrays)
+
+
+def _top_stats(res, stats, total, return_arrays):
     c = res.counts()
     stats.continuation_paths = total
     stats.at_infinity = c["at_infinity"]
@@ -125,6 +139,32 @@ def solve_top(emb: EmbeddedSystem, p: int = 1, seed: int | None = None, params: 
     if stats.continuation_paths and stats.finite == 0:
         raise RuntimeError("all continuation paths failed")
     return (res if return_arrays else res.path_results()), stats
+
+
+def _solve_top_polyhedral(emb, seed, params, cells, cell_log, return_arrays):
+    from . import polyhedral as ph
+
+    seed = emb.seed if seed is None else seed
+    system = emb.system if emb.k > 0 else emb.base
+    cells = list(cells)
+    supports = ph.supports_of(system)
+    g = ph.random_coefficient_system(supports, system.nvars, seed)
+    stats = TopStats()
+    stats.cells = len(cells)
+    stats.mixed_volume = int(sum(int(c.volume) for c in cells))
+    if cell_log is not None:
+        cell_log.extend(cells)
+    t0 = time.perf_counter()
+    start, _ = ph.track_cells(cells, g, supports, params)
+    stats.time_start_system = time.perf_counter() - t0
+    ok = start.succeeded
+    stats.start_paths = len(start)
+    stats.start_failures = int(len(start) - ok.sum())
+    h = LinearHomotopy(g, system, rngmod.gamma_for(seed))
+    t0 = time.perf_counter()
+    res = track_batch(h, start.x[ok], params)
+    stats.time_continuation = time.perf_counter() - t0
+    return _top_stats(res, stats, int(ok.sum()), return_arrays)
 
 
 def _classify_arrays(x: np.ndarray, status_ok: np.ndarray, n_at_inf: int, n_fail: int, emb_level: EmbeddedSystem,

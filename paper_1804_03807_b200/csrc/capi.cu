@@ -734,9 +734,8 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   memset(&g_counters, 0, sizeof(g_counters));
   if (P == 0) return 0;
   if (!starts && !degrees) FAIL("need explicit starts or total-degree degrees");
-  if (h->tw && (!h->ptab || h->jit_kernel || getenv("NID_NO_PTAB")))
-    FAIL("polyhedral homotopy: only the parameter-bank tracker (<= 256 terms, <= 1536 variable occurrences) "
-         "evaluates t-weighted coefficients");
+  if (h->tw && (h->jit_kernel || h->rec))
+    FAIL("polyhedral homotopy: the JIT and streamed-record trackers do not evaluate t-weighted coefficients");
   if (h->tw && !starts) FAIL("polyhedral homotopy: explicit (binomial) start points are required");
   if (h->nparam > 0 && !params) FAIL("homotopy has per-path parameters but none were given");
   if (param_div < 1) param_div = 1;

@@ -639,6 +639,11 @@ struct TableEval {
     rows::eval_rows_fac<N>(H, g, xs, t, prm, aug, part, want_scale, axw);
 #endif
   }
+  // per-cell polyhedral homotopy: tws = the slot's t-exponent row
+  static NID_D void rows(const HomDev& H, int g, const cd (&x)[N], double t, const cd* prm, cd* aug, double* part,
+                         bool want_scale, const cd* xs, double* axw, const double* tws) {
+    rows::eval_rows_fac<N>(H, g, xs, t, prm, aug, part, want_scale, axw, tws);
+  }
 };
 
 // true for the table evaluator (the streamed-record path replaces it for n > 10)
@@ -762,8 +767,17 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
 #pragma unroll
         for (int v = 0; v < N; ++v) x[v] = cb[(L::XE + v) * S + lane];
         const long long pr = lb[S + lane];
-        const cd* prm = pr >= 0 ? Ar.params + pr : nullptr;
-        Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);
+        const cd* prm = (Ar.params && pr >= 0) ? Ar.params + pr : nullptr;
+        const double* tws = Ar.H.tw ? (Ar.ptw ? Ar.ptw + pr : Ar.H.tw) : nullptr;
+        if constexpr (has_table_flag<Eval>::value) {
+          if (tws) {
+            Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane, tws);
+          } else {
+            Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);
+          }
+        } else {
+          Eval::rows(Ar.H, g, x, W_DS(D_TE), prm, aug, part, want, cb + L::XE * S + lane, db + L::AXW * S + lane);
+        }
       }
     }
     NID_TP(2);  // evaluation

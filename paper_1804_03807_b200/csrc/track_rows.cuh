@@ -288,7 +288,7 @@ NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const doub
 // of the cyclic systems): one dispatch per run.  Returns the next term.
 template <int N, int K, bool ML>
 NID_D int fterm_run(const HomDev& H, int k, int k1, uint4 f, const cd* xs, const double* axs, bool ws, cd alpha,
-                    double t, const cd* prm, cd* row, cd& hv, double& sS, double& sT) {
+                    double t, const cd* prm, cd* row, cd& hv, double& sS, double& sT, const double* tws) {
   const int kend = (int)f.w;  // the run's end, precomputed on the host
 #pragma unroll 1
   for (;;) {
@@ -299,10 +299,13 @@ NID_D int fterm_run(const HomDev& H, int k, int k1, uint4 f, const cd* xs, const
       const int sl = __ldg(H.pslot + k);
       if (sl >= 0) ct = prm[sl];
     }
-    const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
+    // tws: polyhedral t-exponents (coefficient ct t^w, polyhedral.py:764-781)
+    const double tp = tws ? pow(t, __ldg(tws + k)) : 1.0;
+    const cd c = tws ? tp * ct : (H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct);
     double m;
     fterm<N, K, ML>(H, k, f, xs, axs, ws, c, row, hv, m);
     if (ws) {
+      if (tws) m = __dmul_rn(m, tp);
       if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
       sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), m));
     }
@@ -314,12 +317,12 @@ NID_D int fterm_run(const HomDev& H, int k, int k1, uint4 f, const cd* xs, const
 
 template <int N, bool ML>
 NID_D int fterm_dispatch(const HomDev& H, int k, int k1, const cd* xs, const double* axs, bool ws, cd alpha, double t,
-                         const cd* prm, cd* row, cd& hv, double& sS, double& sT) {
+                         const cd* prm, cd* row, cd& hv, double& sS, double& sT, const double* tws) {
   const uint4 f = __ldg(H.fac + k);
   switch (f.z) {
 #define NID_FT(KK) \
   case KK:         \
-    if (KK <= N) return fterm_run<N, (KK <= N ? KK : 1), ML>(H, k, k1, f, xs, axs, ws, alpha, t, prm, row, hv, sS, sT); \
+    if (KK <= N) return fterm_run<N, (KK <= N ? KK : 1), ML>(H, k, k1, f, xs, axs, ws, alpha, t, prm, row, hv, sS, sT, tws); \
     break;
     NID_FT(1) NID_FT(2) NID_FT(3) NID_FT(4) NID_FT(5) NID_FT(6) NID_FT(7) NID_FT(8)
     NID_FT(9) NID_FT(10) NID_FT(11) NID_FT(12) NID_FT(13) NID_FT(14) NID_FT(15) NID_FT(16)
@@ -333,11 +336,12 @@ NID_D int fterm_dispatch(const HomDev& H, int k, int k1, const cd* xs, const dou
     const int sl = __ldg(H.pslot + k);
     if (sl >= 0) ct = prm[sl];
   }
-  const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
+  const double tp = tws ? pow(t, __ldg(tws + k)) : 1.0;
+  const cd c = tws ? tp * ct : (H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct);
   hv = cfma(c, cd{1.0, 0.0}, hv);
   if (ws) {
-    if (!H.td) sS = __dadd_rn(sS, __ldg(H.acs + k));
-    sT = __dadd_rn(sT, __ldg(H.act + k));
+    if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), tp));
+    sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), tp));
   }
   return k + 1;
 }
@@ -347,7 +351,7 @@ NID_D int fterm_dispatch(const HomDev& H, int k, int k1, const cd* xs, const dou
 // warp's |x_v| scratch for the slot.
 template <int N>
 NID_D void eval_rows_fac(const HomDev& H, int g, const cd* xs, double t, const cd* prm, cd* aug, double* dbl,
-                         bool want_scale, double* axw) {
+                         bool want_scale, double* axw, const double* tws = nullptr) {
   using L = Layout<N>;
   const cd alpha = (1.0 - t) * H.gamma;
   const bool ws = __any_sync(__activemask(), want_scale);
@@ -365,9 +369,9 @@ NID_D void eval_rows_fac(const HomDev& H, int g, const cd* xs, double t, const c
 #pragma unroll 1
     for (int k = k0; k < k1;) {
       if (H.multilinear) {
-        k = fterm_dispatch<N, true>(H, k, k1, xs, axw, ws, alpha, t, prm, row, hv, sS, sT);
+        k = fterm_dispatch<N, true>(H, k, k1, xs, axw, ws, alpha, t, prm, row, hv, sS, sT, tws);
       } else {
-        k = fterm_dispatch<N, false>(H, k, k1, xs, axw, ws, alpha, t, prm, row, hv, sS, sT);
+        k = fterm_dispatch<N, false>(H, k, k1, xs, axw, ws, alpha, t, prm, row, hv, sS, sT, tws);
       }
     }
     if (H.td) {  // G_i = x_i^{d_i} - 1 in closed form
@@ -389,7 +393,7 @@ NID_D void eval_rows_fac(const HomDev& H, int g, const cd* xs, double t, const c
     }
     row[N * SLOTS] = -hv;
     r2 = nanmax(r2, cabs2(hv));
-    mS = fmax(mS, sS);
+    mS = fmax(mS, tws ? sT : sS);  // polyhedral: one weighted system, (1-t) mT + t mT
     mT = fmax(mT, sT);
   }
   dbl[(L::R2 + g) * SLOTS] = r2;

@@ -259,3 +259,18 @@ def solve_cells(cells, g, supports, params: TrackParams = TrackParams(), mode: s
         raise ValueError(f"unknown mode {mode!r}: this package tracks on the GPU")
     res, _ = track_cells(cells, g, supports, params)
     return res.path_results()
+
+
+def random_coefficient_system(supports, nvars: int, seed: int):
+    """Unit-modulus random coefficients on exactly the given supports, drawn
+    from the reference's START_COEFFS stream (polyhedral.py:645-652), so the
+    same seed gives the same start system g on both sides."""
+    from . import rng as rngmod
+    from .polys import PolySystem, make_poly
+
+    gen = rngmod.stream(seed, rngmod.START_COEFFS)
+    polys = []
+    for pts in supports:
+        coeffs = rngmod.unit_complex(gen, len(pts))
+        polys.append(make_poly(nvars, list(zip(pts, coeffs))))
+    return PolySystem(nvars, tuple(polys))

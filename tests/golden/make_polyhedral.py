@@ -78,6 +78,38 @@ def one(name, system, seed):
     np.savez_compressed(os.path.join(HERE, f"polyhedral_{name}.npz"), **out)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and os.environ.get("POLY_CELLS", "1") == "1":
     one("c1", ref_sys(configs.c1().target), 11)
     one("c2", ref_sys(configs.c2().target), 12)
+
+
+def top(name, pd):
+    """The reference's solve_top with its default polyhedral start
+    (cascade.py:214-246, solve_start_system :110-160) on an embedding: the
+    cells it enumerated (cell_log), its start solutions and continuation
+    results."""
+    import nidpipe.cascade as rc
+
+    from make_golden import ref_emb
+
+    emb = ref_emb(pd.emb)
+    log = []
+    t0 = time.time()
+    res, stats = rc.solve_top(emb, p=1, cell_log=log)
+    print(f"{name}: {stats.cells} cells, mixed volume {stats.mixed_volume}, finite {stats.finite}, "
+          f"at_inf {stats.at_infinity}, failures {stats.failures} in {time.time() - t0:.1f}s")
+    n = emb.system.nvars
+    out = dict(n=np.int32(n), ncells=np.int32(len(log)), cells=np.int32(stats.cells),
+               mixed_volume=np.int64(stats.mixed_volume), start_failures=np.int32(stats.start_failures),
+               finite=np.int32(stats.finite), at_infinity=np.int32(stats.at_infinity),
+               failures=np.int32(stats.failures))
+    for ci, cell in enumerate(log):
+        out[f"c{ci}_pairs"] = np.array([[a, b] for a, b in cell.pairs], np.int32)
+        out[f"c{ci}_texps"] = np.concatenate([np.asarray(t, float) for t in cell.texps])
+        out[f"c{ci}_volume"] = np.int32(cell.volume)
+    out.update({"top_" + k: v for k, v in pack_results(res, n).items()})
+    np.savez_compressed(os.path.join(HERE, f"polyhedral_top_{name}.npz"), **out)
+
+
+if __name__ == "__main__" and os.environ.get("POLY_TOP", "1") == "1":
+    top("c3m", configs.c3_mini())

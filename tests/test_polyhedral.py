@@ -169,3 +169,51 @@ def test_gpu_batched_cells_match_reference(nid, name):
     for x in X[::7]:
         assert np.max(np.abs(O.eval_system(gs, x))) <= 1e-8
     assert len(PH.solve_cells(cells, gs, supports)) == sum(counts)
+
+
+@pytest.mark.parametrize("name,seed", [("c1", 11), ("c2", 12)])
+def test_random_coefficient_system_matches_reference(name, seed):
+    """g from the START_COEFFS stream equals the reference's g (polyhedral.py:645-652)."""
+    g, gs, supports, cells = load(name)
+    mine = PH.random_coefficient_system(supports, gs.nvars, seed)
+    for pa, pb in zip(mine.polys, gs.polys):
+        assert [e for e, _ in pa.terms] == [e for e, _ in pb.terms]
+        np.testing.assert_array_equal([c for _, c in pa.terms], [c for _, c in pb.terms])
+
+
+def load_top(name):
+    g = golden(f"polyhedral_top_{name}")
+    n = int(g["n"])
+    cells = []
+    for c in range(int(g["ncells"])):
+        pr = g[f"c{c}_pairs"]
+        tx = g[f"c{c}_texps"]
+        # split the concatenated t-exponents by each support's size (the
+        # support of row i has len(cell.texps[i]) points)
+        cells.append((pr, tx, int(g[f"c{c}_volume"])))
+    return g, n, cells
+
+
+@pytest.mark.gpu
+def test_gpu_solve_top_polyhedral_matches_reference(nid):
+    """solve_top with the reference's default polyhedral start on the C3-mini
+    embedding (6 variables, 20 cells, mixed volume 256): cell counts, the
+    continuation's finite / at-infinity / failed counts exact, finite
+    endpoints matched as sets within 1e-8."""
+    from paper_1804_03807_b200 import cascade, configs
+
+    g, n, raw = load_top("c3m")
+    pd = configs.c3_mini()
+    system = pd.emb.system
+    supports = PH.supports_of(system)
+    sizes = [len(s) for s in supports]
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    cells = [PH.Cell(tuple((tuple(map(int, pr[i, 0])), tuple(map(int, pr[i, 1]))) for i in range(n)),
+                     tuple(tuple(tx[off[i]:off[i + 1]]) for i in range(n)), vol) for pr, tx, vol in raw]
+    res, stats = cascade.solve_top(pd.emb, cells=cells, return_arrays=True)
+    assert stats.cells == int(g["cells"]) and stats.mixed_volume == int(g["mixed_volume"])
+    assert stats.start_failures == int(g["start_failures"])
+    assert (stats.finite, stats.at_infinity, stats.failures) == (int(g["finite"]), int(g["at_infinity"]),
+                                                                  int(g["failures"]))
+    ref_ok = (g["top_status"] == 0) | (g["top_status"] == 2)
+    match_sets(res.x[res.succeeded], g["top_x"][ref_ok])
