@@ -120,7 +120,7 @@ def solve_top(emb: EmbeddedSystem, p: int = 1, seed: int | None = None, params: 
     launch (`polyhedral.track_cells`), then g -> system from g's roots."""
     _check_mode(mode)
     if cells is not None:
-        return _solve_top_polyhedral(emb, seed, params, cells, cell_log, return_arrays)
+        return _solve_top_polyhedral(emb, seed, params, cells, cell_log, return_arrays, p)
     h, degrees = top_homotopy(emb, seed)
     total = int(np.prod(degrees, dtype=np.int64))
     stats = TopStats(start_paths=total)
@@ -141,30 +141,47 @@ def _top_stats(res, stats, total, return_arrays):
     return (res if return_arrays else res.path_results()), stats
 
 
-def _solve_top_polyhedral(emb, seed, params, cells, cell_log, return_arrays):
+def _solve_top_polyhedral(emb, seed, params, cells, cell_log, return_arrays, p=1):
+    """p >= 2: cells stream through the producer -> GPU consumer pipeline
+    (polyhedral.pipeline_cells; the reference's _pipelined_cells,
+    cascade.py:163-211), so a lazy cell enumeration overlaps the tracking."""
     from . import polyhedral as ph
 
     seed = emb.seed if seed is None else seed
     system = emb.system if emb.k > 0 else emb.base
-    cells = list(cells)
     supports = ph.supports_of(system)
     g = ph.random_coefficient_system(supports, system.nvars, seed)
     stats = TopStats()
-    stats.cells = len(cells)
-    stats.mixed_volume = int(sum(int(c.volume) for c in cells))
-    if cell_log is not None:
-        cell_log.extend(cells)
+    seen: list = []
+
+    def tee():
+        for c in cells:
+            seen.append(c)
+            yield c
+
     t0 = time.perf_counter()
-    start, _ = ph.track_cells(cells, g, supports, params)
+    if p >= 2:
+        rows, _, pst = ph.pipeline_cells(tee(), g, supports, params)
+        if pst.producer_error:
+            raise RuntimeError(f"cell producer failed:\n{pst.producer_error}")
+        x0 = np.array([r.endpoint.coordinates for r in rows if r.succeeded and r.endpoint is not None],
+                      np.complex128).reshape(-1, system.nvars)
+        stats.start_paths = len(rows)
+    else:
+        start, _ = ph.track_cells(list(tee()), g, supports, params)
+        x0 = start.x[start.succeeded]
+        stats.start_paths = len(start)
     stats.time_start_system = time.perf_counter() - t0
-    ok = start.succeeded
-    stats.start_paths = len(start)
-    stats.start_failures = int(len(start) - ok.sum())
+    stats.cells = len(seen)
+    stats.mixed_volume = int(sum(int(c.volume) for c in seen))
+    if cell_log is not None:
+        cell_log.extend(seen)
+    stats.start_failures = int(stats.start_paths - len(x0))
     h = LinearHomotopy(g, system, rngmod.gamma_for(seed))
     t0 = time.perf_counter()
-    res = track_batch(h, start.x[ok], params)
+    res = track_batch(h, x0, params)
     stats.time_continuation = time.perf_counter() - t0
-    return _top_stats(res, stats, int(ok.sum()), return_arrays)
+    return _top_stats(res, stats, len(x0), return_arrays)
 
 
 def _classify_arrays(x: np.ndarray, status_ok: np.ndarray, n_at_inf: int, n_fail: int, emb_level: EmbeddedSystem,

@@ -274,3 +274,124 @@ def random_coefficient_system(supports, nvars: int, seed: int):
         coeffs = rngmod.unit_complex(gen, len(pts))
         polys.append(make_poly(nvars, list(zip(pts, coeffs))))
     return PolySystem(nvars, tuple(polys))
+
+
+# ---------------------------------------------------------------- pipeline
+
+
+@dataclass
+class PipelineStats:
+    """parallel.py:156-164, plus the GPU consumer's batch count."""
+
+    produced: int = 0
+    consumed: int = 0
+    batches: int = 0
+    makespan: float = 0.0
+    producer_blocked: float = 0.0
+    consumer_idle: float = 0.0
+    first_consume_before_last_produce: bool = False
+    producer_error: str | None = None
+
+
+def pipeline_cells(producer, g, supports, params: TrackParams = TrackParams(), queue_capacity: int = 64,
+                   max_batch_cells: int = 4096, track=None):
+    """Cell producer -> GPU consumer pipeline (the paper's pipelining of
+    cell enumeration with path tracking; the reference's `_pipelined_cells`
+    cascade.py:163-211 over `pipeline_run` parallel.py:166-231).
+
+    The producer (any iterable of cells -- e.g. the reference's CPU LP
+    enumeration feeding a queue) runs in its own thread behind a bounded
+    queue.  ONE consumer thread owns the GPU: it blocks for the first
+    available cell, drains whatever else is queued (up to max_batch_cells)
+    and tracks that batch in one launch (`track_cells`); the C call releases
+    the GIL, so enumeration continues while the GPU tracks.  A producer error
+    closes the queue; what was produced is still tracked and the error is
+    reported in the stats, as in the reference.
+
+    Returns (list of PathResult in cell order, per-cell path counts,
+    PipelineStats).  `track(cells, g, supports, params) -> (TrackResults,
+    counts)` replaces the GPU call in host-logic tests."""
+    import queue
+    import threading
+    import time
+    import traceback
+
+    if queue_capacity < 1:
+        raise ValueError("queue capacity must be positive")
+    track = track or track_cells
+    stats = PipelineStats()
+    buf: queue.Queue = queue.Queue(maxsize=queue_capacity)
+    done = object()
+    per_cell: dict = {}
+    produce_done_at = [None]
+    first_consume_at = [None]
+    consumer_error: list = []
+
+    def produce():
+        idx = 0
+        try:
+            for cell in producer:
+                t0 = time.perf_counter()
+                buf.put((idx, cell))
+                stats.producer_blocked += time.perf_counter() - t0
+                idx += 1
+        except Exception:  # noqa: BLE001 -- reported, as parallel.py:199-200
+            stats.producer_error = traceback.format_exc(limit=4)
+        finally:
+            stats.produced = idx
+            produce_done_at[0] = time.perf_counter()
+            buf.put(done)
+
+    def consume():
+        finished = False
+        while not finished:
+            t0 = time.perf_counter()
+            got = buf.get()
+            stats.consumer_idle += time.perf_counter() - t0
+            if got is done:
+                return
+            batch = [got]
+            while len(batch) < max_batch_cells:
+                try:
+                    nxt = buf.get_nowait()
+                except queue.Empty:
+                    break
+                if nxt is done:
+                    finished = True
+                    break
+                batch.append(nxt)
+            if first_consume_at[0] is None:
+                first_consume_at[0] = time.perf_counter()
+            try:
+                res, counts = track([c for _, c in batch], g, supports, params)
+            except Exception:  # noqa: BLE001 -- re-raised on the calling thread
+                consumer_error.append(traceback.format_exc(limit=6))
+                while not finished and buf.get() is not done:  # unblock the producer
+                    pass
+                return
+            rows = res.path_results()
+            pos = 0
+            for (i, _), k in zip(batch, counts):
+                per_cell[i] = (rows[pos:pos + k], k)
+                pos += k
+            stats.batches += 1
+
+    t_start = time.perf_counter()
+    pt = threading.Thread(target=produce, name="nid-cell-producer")
+    ct = threading.Thread(target=consume, name="nid-gpu-consumer")
+    pt.start()
+    ct.start()
+    pt.join()
+    ct.join()
+    stats.makespan = time.perf_counter() - t_start
+    if consumer_error:
+        raise RuntimeError(f"GPU consumer failed:\n{consumer_error[0]}")
+    stats.consumed = len(per_cell)
+    if first_consume_at[0] is not None and produce_done_at[0] is not None:
+        stats.first_consume_before_last_produce = first_consume_at[0] < produce_done_at[0]
+    results, counts = [], []
+    for i in sorted(per_cell):
+        rows, k = per_cell[i]
+        results.extend(rows)
+        counts.append(k)
+    return results, counts, stats

@@ -195,7 +195,8 @@ def load_top(name):
 
 
 @pytest.mark.gpu
-def test_gpu_solve_top_polyhedral_matches_reference(nid):
+@pytest.mark.parametrize("p", [1, 2])
+def test_gpu_solve_top_polyhedral_matches_reference(nid, p):
     """solve_top with the reference's default polyhedral start on the C3-mini
     embedding (6 variables, 20 cells, mixed volume 256): cell counts, the
     continuation's finite / at-infinity / failed counts exact, finite
@@ -210,10 +211,97 @@ def test_gpu_solve_top_polyhedral_matches_reference(nid):
     off = np.concatenate([[0], np.cumsum(sizes)])
     cells = [PH.Cell(tuple((tuple(map(int, pr[i, 0])), tuple(map(int, pr[i, 1]))) for i in range(n)),
                      tuple(tuple(tx[off[i]:off[i + 1]]) for i in range(n)), vol) for pr, tx, vol in raw]
-    res, stats = cascade.solve_top(pd.emb, cells=cells, return_arrays=True)
+    # p = 2: the cells stream through the producer -> GPU consumer pipeline
+    res, stats = cascade.solve_top(pd.emb, p=p, cells=iter(cells), return_arrays=True)
     assert stats.cells == int(g["cells"]) and stats.mixed_volume == int(g["mixed_volume"])
     assert stats.start_failures == int(g["start_failures"])
     assert (stats.finite, stats.at_infinity, stats.failures) == (int(g["finite"]), int(g["at_infinity"]),
                                                                   int(g["failures"]))
     ref_ok = (g["top_status"] == 0) | (g["top_status"] == 2)
     match_sets(res.x[res.succeeded], g["top_x"][ref_ok])
+
+
+# ------------------------------------------------------------- pipeline
+
+
+class _FakeResults:
+    def __init__(self, rows):
+        self.rows = rows
+
+    def path_results(self):
+        return self.rows
+
+
+def _fake_track(delay=0.0, fail_on=None):
+    calls = []
+
+    def track(cells, g, supports, params):
+        import time
+
+        calls.append(len(cells))
+        if fail_on is not None and any(c == fail_on for c in cells):
+            raise ValueError("boom")
+        time.sleep(delay)
+        rows = [(c, j) for c in cells for j in range(c % 3 + 1)]
+        return _FakeResults(rows), [c % 3 + 1 for c in cells]
+
+    return track, calls
+
+
+def test_pipeline_keeps_cell_order_and_batches():
+    import time
+
+    def slow_cells():
+        for c in range(40):
+            time.sleep(0.002)
+            yield c
+
+    track, calls = _fake_track(delay=0.01)
+    res, counts, st = PH.pipeline_cells(slow_cells(), None, (), track=track, queue_capacity=4)
+    assert counts == [c % 3 + 1 for c in range(40)]
+    assert res == [(c, j) for c in range(40) for j in range(c % 3 + 1)]
+    assert st.produced == st.consumed == 40 and sum(calls) == 40 and st.batches == len(calls)
+    assert st.first_consume_before_last_produce and st.producer_error is None
+
+
+def test_pipeline_producer_error_is_reported_and_drained():
+    def bad_cells():
+        yield 1
+        yield 2
+        raise RuntimeError("lp failed")
+
+    track, _ = _fake_track()
+    res, counts, st = PH.pipeline_cells(bad_cells(), None, (), track=track)
+    assert st.produced == 2 and st.consumed == 2 and counts == [2, 3]
+    assert "lp failed" in st.producer_error
+
+
+def test_pipeline_consumer_error_raises():
+    track, _ = _fake_track(fail_on=5)
+    with pytest.raises(RuntimeError, match="GPU consumer failed"):
+        PH.pipeline_cells(iter(range(200)), None, (), track=track, queue_capacity=2, max_batch_cells=1)
+
+
+@pytest.mark.gpu
+def test_gpu_pipeline_matches_reference_c2(nid):
+    """C2's 115 cells streamed by a producer thread (with the pauses of a
+    CPU enumeration) through the GPU consumer: per-cell parity."""
+    import time
+
+    g, gs, supports, cells = load("c2")
+
+    def producer():
+        for c in cells:
+            time.sleep(0.001)
+            yield c
+
+    res, counts, st = PH.pipeline_cells(producer(), gs, supports, queue_capacity=16)
+    assert counts == [c.volume for c in cells] and st.consumed == len(cells) and st.batches >= 2
+    pos = 0
+    for c, k in enumerate(counts):
+        st_c = np.array([STATUS[r.status] for r in res[pos:pos + k]])
+        assert np.array_equal(np.sort(st_c), np.sort(g[f"c{c}_status"])), c
+        ok = g[f"c{c}_status"] == 0
+        match_sets(np.array([r.endpoint.coordinates for r in res[pos:pos + k] if r.status == "converged"]),
+                   g[f"c{c}_x"][ok])
+        pos += k

@@ -42,5 +42,28 @@ def main():
               f"{res.counters.get('kernel_ms_track', float('nan')):.2f} ms), mean steps {np.mean(res.steps):.1f}")
 
 
+def pipeline(lp_ms: float = 18.0):
+    """C2 with a producer that pays lp_ms per cell (the reference's CPU LP
+    enumerates C2's 115 cells in ~2.1 s, i.e. ~18 ms per cell): the
+    pipeline's makespan against enumerate-all-then-track."""
+    g, gs, supports, cells = load("c2")
+
+    def producer():
+        for c in cells:
+            time.sleep(lp_ms * 1e-3)
+            yield c
+
+    t0 = time.perf_counter()
+    allc = list(producer())
+    PH.track_cells(allc, gs, supports)
+    seq = time.perf_counter() - t0
+    res, counts, st = PH.pipeline_cells(producer(), gs, supports)
+    conv = sum(1 for r in res if r.status == "converged")
+    print(f"c2 pipeline (LP {lp_ms} ms/cell): sequential {seq * 1e3:.0f} ms, pipelined {st.makespan * 1e3:.0f} ms "
+          f"({st.batches} batches, consumer idle {st.consumer_idle * 1e3:.0f} ms, converged {conv}, "
+          f"first consume before last produce: {st.first_consume_before_last_produce})")
+
+
 if __name__ == "__main__":
     main()
+    pipeline()
