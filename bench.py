@@ -262,7 +262,7 @@ def native_arm(args, prob):
                          f"(numpy restatement of nidpipe.tracker.track) on {cores} processes"}
 
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "track_traffic_r01v.json")
+    tp = os.path.join(ROOT, "profiles", "track_traffic_r01ff.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
