@@ -37,6 +37,10 @@ static int g_device = -1;
     }                                                                                     \
   } while (0)
 
+// the ABI the ctypes mirror (paper_1804_03807_b200/_lib.py) and tests/test_host.py pin
+static_assert(sizeof(NidHomotopyDesc) == 96, "NidHomotopyDesc layout changed");
+static_assert(sizeof(NidTrackParams) == 96, "NidTrackParams layout changed");
+
 struct NidHomotopy {
   int n, nterms, nparam, maxdeg, multilinear, td;
   int tddeg[NID_MAX_VARS];
