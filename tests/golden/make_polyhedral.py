@@ -113,3 +113,36 @@ def top(name, pd):
 
 if __name__ == "__main__" and os.environ.get("POLY_TOP", "1") == "1":
     top("c3m", configs.c3_mini())
+
+
+def decompose_golden(name, pd):
+    """The reference's decompose (blackbox.py:36-110; polyhedral start,
+    cascade, filter_junk, classify_isolated) on a base system: its cell log
+    and the decomposition's counts."""
+    import nidpipe.blackbox as rb
+
+    f = ref_sys(pd.f)
+    log = []
+    t0 = time.time()
+    rep = rb.decompose(f, top_dimension=pd.emb.k, seed=pd.seed, tasks=1, mode="thread", cell_log=log)
+    print(f"{name} decompose: degrees {rep.degrees}, isolated {len(rep.isolated)}, suspects {len(rep.suspects)}, "
+          f"cascade {rep.cascade_counts} in {time.time() - t0:.1f}s")
+    n = pd.emb.system.nvars
+    out = dict(n=np.int32(n), ncells=np.int32(len(log)),
+               degrees=np.array(sorted(rep.degrees.items()), np.int64).reshape(-1, 2),
+               isolated=np.array([s.coordinates for s in rep.isolated], np.complex128).reshape(-1, pd.f.nvars),
+               suspects=np.int32(len(rep.suspects)),
+               cascade=np.array([[c.get(k, 0) for k in ("dimension", "starts", "at_infinity", "zero_slack",
+                                                         "nonzero_slack", "failures")] for c in rep.cascade_counts],
+                                np.int64),
+               stages=np.array([[s.candidate_dimension, s.against_dimension, s.candidates, s.removed]
+                                for s in rep.filter_stages], np.int64).reshape(-1, 4))
+    for ci, cell in enumerate(log):
+        out[f"c{ci}_pairs"] = np.array([[a, b] for a, b in cell.pairs], np.int32)
+        out[f"c{ci}_texps"] = np.concatenate([np.asarray(t, float) for t in cell.texps])
+        out[f"c{ci}_volume"] = np.int32(cell.volume)
+    np.savez_compressed(os.path.join(HERE, f"decompose_{name}.npz"), **out)
+
+
+if __name__ == "__main__" and os.environ.get("POLY_DECOMPOSE", "0") == "1":
+    decompose_golden("c3m", configs.c3_mini())

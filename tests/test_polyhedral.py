@@ -305,3 +305,71 @@ def test_gpu_pipeline_matches_reference_c2(nid):
         match_sets(np.array([r.endpoint.coordinates for r in res[pos:pos + k] if r.status == "converged"]),
                    g[f"c{c}_x"][ok])
         pos += k
+
+
+# ------------------------------------------------------------- decompose
+
+
+def _cells_from(g, n, system):
+    supports = PH.supports_of(system)
+    off = np.concatenate([[0], np.cumsum([len(s) for s in supports])])
+    cells = []
+    for c in range(int(g["ncells"])):
+        pr = g[f"c{c}_pairs"]
+        tx = g[f"c{c}_texps"]
+        cells.append(PH.Cell(tuple((tuple(map(int, pr[i, 0])), tuple(map(int, pr[i, 1]))) for i in range(n)),
+                             tuple(tuple(tx[off[i]:off[i + 1]]) for i in range(n)), int(g[f"c{c}_volume"])))
+    return cells
+
+
+def test_decompose_argument_checks():
+    from paper_1804_03807_b200 import blackbox, configs
+
+    f = configs.c3_mini().f
+    with pytest.raises(ValueError):
+        blackbox.decompose(f, top_dimension=f.nvars, cells=[])
+    with pytest.raises(ValueError):
+        blackbox.decompose(f, top_dimension=2, precision="dd", cells=[])
+    with pytest.raises(ValueError):
+        blackbox.decompose(f, top_dimension=2, mode="thread", cells=[])
+    nonsquare = PolySystem(f.nvars, f.polys[:-1])
+    with pytest.raises(ValueError):
+        blackbox.decompose(nonsquare, top_dimension=2, cells=[])
+
+
+@pytest.mark.gpu
+def test_gpu_decompose_matches_reference_c3m(nid):
+    """decompose(mode="gpu") from the polyhedral start (the reference's cell
+    log) on the C3-mini base system against the reference's own decompose:
+    witness-set degrees, cascade counts, filter stages and isolated points."""
+    from paper_1804_03807_b200 import blackbox, configs
+
+    g = golden("decompose_c3m")
+    pd = configs.c3_mini()
+    cells = _cells_from(g, int(g["n"]), pd.emb.system)
+    rep = blackbox.decompose(pd.f, top_dimension=pd.emb.k, seed=pd.seed, cells=cells)
+    assert sorted(rep.degrees.items()) == [tuple(r) for r in g["degrees"].tolist()]
+    keys = ("dimension", "starts", "at_infinity", "zero_slack", "nonzero_slack", "failures")
+    assert [[c[k] for k in keys] for c in rep.cascade_counts] == g["cascade"].tolist()
+    # stage shapes exact; junk removal checked as in test_gpu_pipeline.py: the
+    # junk candidates lie on a positive-dimensional set, so where a cascade
+    # path lands on it depends on rounding history -- every GPU verdict must
+    # equal the CPU oracle's verdict on the same candidate
+    assert [[s.candidate_dimension, s.against_dimension, s.candidates]
+            for s in rep.filter_stages] == [r[:3] for r in g["stages"].tolist()]
+    from paper_1804_03807_b200 import filtering
+
+    n = pd.emb.n_original
+    wpts = [s.coordinates for s in rep.witness_sets[0].points]
+    for st in rep.filter_stages:
+        if st.candidate_dimension == 0:
+            continue
+        lv = [lv for lv in rep.superset.levels if lv.dimension == st.candidate_dimension][0]
+        Q = [c.coordinates[:n] for c in filtering._dedup(list(lv.zero_slack), n)]
+        assert st.removed == sum(O.membership_test(wpts, pd.emb, q) for q in Q)
+    ref0 = [r for r in g["stages"].tolist() if r[0] == 0]
+    assert [[s.candidate_dimension, s.against_dimension, s.candidates, s.removed]
+            for s in rep.filter_stages if s.candidate_dimension == 0] == ref0
+    assert len(rep.suspects) == int(g["suspects"])
+    iso = np.array([s.coordinates for s in rep.isolated]).reshape(-1, pd.f.nvars)
+    match_sets(iso, g["isolated"])
