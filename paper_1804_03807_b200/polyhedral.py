@@ -135,30 +135,34 @@ class PolyhedralHomotopy:
 
 def _hermite_lower(V):
     """(L, U): U unimodular, L = V U lower triangular with a positive
-    diagonal.  Column Euclid row by row; exact integer arithmetic."""
+    diagonal.  Column Euclid row by row; exact integer arithmetic on plain
+    Python ints (columns stored as lists)."""
     n = len(V)
-    M = np.array(V, dtype=object).reshape(n, n)
-    U = np.eye(n, dtype=np.int64).astype(object)
+    Mc = [[int(V[r][c]) for r in range(n)] for c in range(n)]  # Mc[c] = column c of M
+    Uc = [[int(r == c) for r in range(n)] for c in range(n)]
     for k in range(n):
         while True:
-            cols = [j for j in range(k, n) if M[k, j] != 0]
+            cols = [j for j in range(k, n) if Mc[j][k] != 0]
             if not cols:
                 raise ValueError("the cell's edge matrix is singular")
-            p = min(cols, key=lambda j: abs(M[k, j]))
+            p = min(cols, key=lambda j: abs(Mc[j][k]))
             if p != k:
-                M[:, [k, p]] = M[:, [p, k]]
-                U[:, [k, p]] = U[:, [p, k]]
-            rest = [j for j in range(k + 1, n) if M[k, j] != 0]
+                Mc[k], Mc[p] = Mc[p], Mc[k]
+                Uc[k], Uc[p] = Uc[p], Uc[k]
+            rest = [j for j in range(k + 1, n) if Mc[j][k] != 0]
             if not rest:
                 break
+            mk, uk, piv = Mc[k], Uc[k], Mc[k][k]
             for j in rest:
-                q = M[k, j] // M[k, k]
-                M[:, j] -= q * M[:, k]
-                U[:, j] -= q * U[:, k]
-        if M[k, k] < 0:
-            M[:, k] = -M[:, k]
-            U[:, k] = -U[:, k]
-    return M, U
+                q = Mc[j][k] // piv
+                Mc[j] = [a - q * b for a, b in zip(Mc[j], mk)]
+                Uc[j] = [a - q * b for a, b in zip(Uc[j], uk)]
+        if Mc[k][k] < 0:
+            Mc[k] = [-a for a in Mc[k]]
+            Uc[k] = [-a for a in Uc[k]]
+    L = np.array(Mc, dtype=np.int64).T
+    U = np.array(Uc, dtype=np.int64).T
+    return L, U
 
 
 def binomial_solutions(V, beta) -> np.ndarray:
@@ -189,10 +193,20 @@ def binomial_solutions(V, beta) -> np.ndarray:
     return Y
 
 
+def _coeff_maps(g):
+    cached = getattr(g, "_cache", None)
+    if isinstance(cached, dict) and "coeff_of" in cached:
+        return cached["coeff_of"]
+    maps = [dict((tuple(int(v) for v in e), complex(c)) for e, c in p.terms) for p in g.polys]
+    if isinstance(cached, dict):
+        cached["coeff_of"] = maps
+    return maps
+
+
 def cell_starts(cell, g) -> np.ndarray:
     """The cell's binomial start system and its roots (polyhedral.py:800-808)."""
     n = g.nvars
-    coeff_of = [dict((tuple(int(v) for v in e), complex(c)) for e, c in p.terms) for p in g.polys]
+    coeff_of = _coeff_maps(g)
     V, beta = [], []
     for i, (a, b) in enumerate(cell.pairs):
         a, b = tuple(int(v) for v in a), tuple(int(v) for v in b)
