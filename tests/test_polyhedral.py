@@ -373,3 +373,47 @@ def test_gpu_decompose_matches_reference_c3m(nid):
     assert len(rep.suspects) == int(g["suspects"])
     iso = np.array([s.coordinates for s in rep.isolated]).reshape(-1, pd.f.nvars)
     match_sets(iso, g["isolated"])
+
+
+# ------------------------------------------------------------- edge cases
+
+
+@pytest.mark.gpu
+def test_gpu_polyhedral_univariate_cell(nid):
+    """n = 1: g = a x^3 + b, one cell (volume 3) whose binomial system is g
+    itself -- the three roots of g, each converged."""
+    a, b = 0.6 - 0.8j, -1.3 + 0.4j
+    g = PolySystem(1, (make_poly(1, [((0,), b), ((3,), a)]),))
+    supports = PH.supports_of(g)
+    cell = PH.Cell((((0,), (3,)),), ((0.0, 0.0),), 3)
+    res = PH.solve_cell(cell, g, supports)
+    roots = np.roots([a, 0, 0, b])
+    X = np.array([r.endpoint.coordinates for r in res if r.status == "converged"])
+    assert len(X) == 3
+    match_sets(X, roots.reshape(-1, 1), 1e-12)
+
+
+@pytest.mark.gpu
+def test_gpu_polyhedral_argument_errors(nid):
+    from paper_1804_03807_b200 import _lib
+    from paper_1804_03807_b200.homotopy import LinearHomotopy
+
+    g, gs, supports, cells = load("c1")
+    with pytest.raises(ValueError):
+        PH.track_cells([], gs, supports)
+    low = PH.lower_polyhedral(gs, cells[0], supports)
+    bad = type(low)(**{**low.__dict__, "texp": -np.ones_like(low.texp)})
+    with pytest.raises(_lib.NidError, match="term_texp"):
+        PH.DeviceHomotopy(bad)
+    # a linear homotopy handle refuses per-cell t-exponent rows
+    h = LinearHomotopy(gs, gs, 1.0 + 0j)
+    import ctypes as C
+
+    L = _lib.lib()
+    st = np.zeros((1, gs.nvars), np.complex128)
+    tw = np.zeros((1, low.nterms))
+    out = np.zeros((1, gs.nvars), np.complex128)
+    o = _lib.PathOutC(_lib.ptr(out), *[None] * 6)
+    rc = L.nid_track_cells(h.device().handle, C.byref(PH.TrackParams().to_c()), 1, _lib.ptr(st), _lib.ptr(tw),
+                           C.byref(o), 0, None)
+    assert rc != 0 and b"polyhedral" in L.nid_last_error()
