@@ -186,7 +186,7 @@ def native_arm(args, prob):
     def step():
         flush.fill_(1.0)
         c = tracker.track_batch_device(h, params, Pl, outp, degrees=prob.degrees, first_index=lo,
-                                       index_stride=stride, stream=stream.cuda_stream, jit=args.jit)
+                                       index_stride=stride, stream=stream.cuda_stream)
         if ctx.world > 1:
             gather_finite(ctx, x_end, status)
         return c
@@ -237,12 +237,12 @@ def native_arm(args, prob):
                                   pin(Pl, torch.float64).numpy(), pin(Pl, torch.float64).numpy(),
                                   pin(Pl, torch.float64).numpy(), pin(Pl, torch.int8).numpy(), {})
         x0v = X0.numpy().view(np.complex128).reshape(Pl, n)
-        tracker.track_batch(h, x0v, params, out=ho, jit=args.jit)  # warm
+        tracker.track_batch(h, x0v, params, out=ho)  # warm
         ctx.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            r = tracker.track_batch(h, x0v, params, out=ho, jit=args.jit)
+            r = tracker.track_batch(h, x0v, params, out=ho)
             _ = int(np.sum(r.succeeded))  # the step's result read on the host
         torch.cuda.synchronize()
         dt = ctx.max_over_ranks(time.perf_counter() - t0)
@@ -282,7 +282,7 @@ def native_arm(args, prob):
             "e2e": e2e,
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "track_ctl_kernel<10, JitEval>" if args.jit else "track_pt_kernel<10, false>",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "track_pt_kernel<10, false>",
                          "peak_source": peak_src,
                          "algorithmic_flop_per_launch": flop, "kernel_ms_per_launch": k_ms,
                          "endpoint_kernel_ms_per_launch": e_ms, "share_of_step": k_ms / (ms / args.steps),
@@ -304,7 +304,6 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--jit", action="store_true", help="NVRTC-specialised evaluator instead of the table kernel")
     ap.add_argument("--cpu-sample", type=int, default=480)
     ap.add_argument("--ref-sample", type=int, default=160)
     args = ap.parse_args()

@@ -168,13 +168,6 @@ int nid_last_counters(NidCounters* c);
 int nid_track_cells(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
                     const double* path_texp, NidPathOut* out, int device_io, void* stream);
 
-/* Compile a homotopy-specialised tracker with NVRTC and attach it to h:
- * `src` is the evaluator source generated by paper_1804_03807_b200/jit.py,
- * `include_dir` the directory of csrc/ and include/ headers (colon separated).
- * Subsequent nid_track_batch calls on h launch the specialised kernel.
- * The compiler log goes to `log` (capacity logcap). */
-int nid_homotopy_jit(NidHomotopy* h, const char* src, const char* include_dirs, char* log, int logcap);
-
 /* newton_refine(f, x, tol, iters) on P points, then classify (n_original,
  * infinity_threshold): x in/out [P*n*2], residual, condition, regular,
  * rank, slack class.  The homotopy is evaluated at t = 1 (target rows). */

@@ -22,7 +22,7 @@ EXPORTS = (
     "nid_last_error", "nid_device_count", "nid_init", "nid_shutdown", "nid_homotopy_create",
     "nid_homotopy_destroy", "nid_eval_batch", "nid_newton_step_batch", "nid_svd_batch",
     "nid_track_batch", "nid_track_batch_strided", "nid_last_counters", "nid_refine_batch", "nid_dd_refine_batch",
-    "nid_match_pairs", "nid_homotopy_jit", "nid_track_cells",
+    "nid_match_pairs", "nid_track_cells",
 )
 
 
@@ -99,7 +99,6 @@ def load_library():
             "nid_dd_refine_batch": ([p, i, p, i, p], i),
             "nid_match_pairs": ([i, i, i, p, p, ll, p], i),
             "nid_track_regs": ([i], i),
-            "nid_homotopy_jit": ([p, C.c_char_p, C.c_char_p, p, i], i),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)

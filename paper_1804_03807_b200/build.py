@@ -81,7 +81,7 @@ def build(jobs: int | None = None, verbose: bool = False, force: bool = False, o
                 if verbose and out.strip():
                     print(out)
     if cmds or force or not os.path.exists(lib) or any(os.path.getmtime(x) > os.path.getmtime(lib) for x in objs):
-        _run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-lnvrtc"])
+        _run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"])
     return lib
 
 

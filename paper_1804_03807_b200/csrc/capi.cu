@@ -1,8 +1,6 @@
 // libnid.so: the C-ABI boundary (declared in include/nid.h).
 // Host-side plumbing only: uploads lowered homotopies, stages host buffers,
 // sizes the persistent grids and dispatches to the per-size kernels.
-#include <nvrtc.h>
-
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -58,14 +56,6 @@ struct NidHomotopy {
   TermRec* rec = nullptr;  // streamed records (csrc/track_rec.cuh), n > 10
   uint4* runs = nullptr;
   int grun[17] = {0};
-  TermRec* srec = nullptr;  // shared-monomial tables (csrc/track_sme.cuh)
-  unsigned long long* smono = nullptr;
-  uint4* schunk = nullptr;
-  unsigned* scnt = nullptr;
-  int snchunk = 0;
-  int sbase[17] = {0};
-  cudaLibrary_t jit_lib = nullptr;  // NVRTC-specialised tracker (nid_homotopy_jit)
-  cudaKernel_t jit_kernel = nullptr;
   HomDev dev() const {
     HomDev h;
     h.n = n;
@@ -91,12 +81,6 @@ struct NidHomotopy {
     h.rec = rec;
     h.runs = runs;
     for (int v = 0; v <= 16; ++v) h.grun[v] = grun[v];
-    h.srec = srec;
-    h.smono = smono;
-    h.schunk = schunk;
-    h.scnt = scnt;
-    h.snchunk = snchunk;
-    for (int v = 0; v <= 16; ++v) h.sbase[v] = sbase[v];
     return h;
   }
 };
@@ -144,7 +128,30 @@ static const EvalFn k_eval[17] = NID_TABLE(launch_eval_);
 static const NewtonFn k_newton[17] = NID_TABLE(launch_newton_);
 static const RegsFn k_regs[17] = NID_TABLE(track_regs_);
 static const RegsFn k_tthreads[17] = NID_TABLE(track_threads_);
-static const RegsFn k_tsmem[17] = NID_TABLE(track_smem_);
+
+// The CUDA current device is per host thread: every entry point that touches
+// the device re-binds the device nid_init chose, so calls from another host
+// thread (e.g. the cell-pipeline consumer, polyhedral.pipeline_cells) land on
+// the same GPU as the workspaces and handles.
+#define BIND()                                                        \
+  do {                                                                \
+    if (g_device >= 0) {                                              \
+      cudaError_t be_ = cudaSetDevice(g_device);                      \
+      if (be_ != cudaSuccess) {                                       \
+        g_err = std::string("cudaSetDevice: ") + cudaGetErrorString(be_); \
+        return 2;                                                     \
+      }                                                               \
+    }                                                                 \
+  } while (0)
+
+// CUDA events destroyed on every exit path
+struct Events {
+  cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+  ~Events() {
+    for (auto& x : e)
+      if (x) cudaEventDestroy(x);
+  }
+};
 
 static int sm_count() {
   int dev = 0, sms = 148;
@@ -181,6 +188,7 @@ int nid_init(int device) {
 }
 
 int nid_shutdown(void) {
+  BIND();
   for (auto& b : g_bufs) {
     if (b.p) cudaFree(b.p);
     b.p = nullptr;
@@ -195,6 +203,7 @@ int nid_track_regs(int n) {
 }
 
 int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
+  BIND();
   if (!d || !out) FAIL("null argument");
   if (d->n < 1 || d->n > NID_MAX_VARS) FAIL("n must be in 1..16");
   if (d->nterms < 0) FAIL("negative term count");
@@ -472,128 +481,6 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
         h->runs = nullptr;
       }
     }
-    // shared-monomial tables (csrc/track_sme.cuh): when the rows share their
-    // monomials (C3/C4: the eight heavy rows have the same 495-monomial
-    // support), each distinct monomial and its partials are formed once per
-    // slot and every row accumulates coefficient x (value, partials).
-    // Opt-in (NID_SME=1): measured slower than the streamed records on C3
-    // (1,475 vs 1,086 ms on the 18,944-path probe).
-    if (!e && h->rec && getenv("NID_SME") && atoi(getenv("NID_SME")) != 0) {
-      const int G = rows::groups_for(n);
-      std::map<std::vector<unsigned char>, int> mid;
-      std::vector<std::vector<unsigned char>> mono;
-      std::vector<int> term_mono(T, -1);
-      bool ok = G == 8;
-      for (int gg = 0; gg < G; ++gg) ok = ok && h->goff[gg + 1] - h->goff[gg] <= 2;  // two rows per warp at most
-      for (int k = 0; k < T && ok; ++k) {
-        std::vector<unsigned char> ex(d->expo + k * NID_MAX_VARS, d->expo + k * NID_MAX_VARS + n);
-        int deg = 0;
-        for (int v = 0; v < n; ++v) deg += ex[v];
-        if (deg == 0) continue;
-        if (deg > SME_KM) ok = false;
-        auto it = mid.find(ex);
-        if (it == mid.end()) {
-          it = mid.emplace(ex, (int)mono.size()).first;
-          mono.push_back(ex);
-        }
-        term_mono[k] = it->second;
-      }
-      const int pairs = T;  // (row, term) pairs
-      ok = ok && !mono.empty() && pairs >= 2 * (int)mono.size();
-      if (ok) {
-        // monomials by degree, chunks of up to G per degree
-        std::vector<int> order(mono.size());
-        for (size_t z = 0; z < order.size(); ++z) order[z] = (int)z;
-        auto degof = [&](int m) {
-          int dd = 0;
-          for (int v = 0; v < n; ++v) dd += mono[m][v];
-          return dd;
-        };
-        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return degof(a) < degof(b); });
-        std::vector<int> pos_of(mono.size());
-        std::vector<uint4> chunks;
-        std::vector<unsigned long long> smono;
-        for (size_t z = 0; z < order.size();) {
-          const int K = degof(order[z]);
-          size_t z1 = z;
-          while (z1 < order.size() && degof(order[z1]) == K && (int)(z1 - z) < G) ++z1;
-          chunks.push_back(make_uint4((unsigned)K, (unsigned)smono.size(), (unsigned)(z1 - z), 0u));
-          for (size_t w = z; w < z1; ++w) {
-            const int m = order[w];
-            pos_of[m] = (int)smono.size();
-            unsigned long long meta = 0;
-            int np = 0;
-            for (int v = 0; v < n; ++v)
-              for (int a = 0; a < mono[m][v]; ++a) {
-                meta |= (unsigned long long)v << (4 * np);
-                if (a > 0) meta |= 1ull << (52 + np);
-                ++np;
-              }
-            meta |= (unsigned long long)np << 48;
-            smono.push_back(meta);
-          }
-          z = z1;
-        }
-        const int NC = (int)chunks.size();
-        // consumer records per warp group: chunk by chunk, the group's rows'
-        // terms whose monomial is in the chunk (constants with chunk 0)
-        std::vector<TermRec> srec;
-        std::vector<unsigned> scnt((size_t)NC * G, 0u);
-        for (int gg = 0; gg < G; ++gg) {
-          h->sbase[gg] = (int)srec.size();
-          for (int c = 0; c < NC; ++c) {
-            const unsigned lo = chunks[c].y, hi = chunks[c].y + chunks[c].z;
-            unsigned cnt = 0;
-            for (int gi = h->goff[gg], li = 0; gi < h->goff[gg + 1]; ++gi, ++li) {
-              const int i = h->grow[gi];
-              for (int k = off[i]; k < off[i + 1]; ++k) {
-                const int m = term_mono[k];
-                const bool cst = m < 0;
-                if (cst ? c != 0 : ((unsigned)pos_of[m] < lo || (unsigned)pos_of[m] >= hi)) continue;
-                TermRec r;
-                memset(&r, 0, sizeof(r));
-                r.ctr = d->coef_target[2 * k];
-                r.cti = d->coef_target[2 * k + 1];
-                r.csr = d->coef_start[2 * k];
-                r.csi = d->coef_start[2 * k + 1];
-                r.acs = acs[k];
-                r.act = act[k];
-                r.meta = cst ? 0ull : smono[pos_of[m]];
-                r.pslot = d->param_slot ? (int)d->param_slot[k] : -1;
-                r.pad = (cst ? 0x100 : (pos_of[m] - (int)lo)) | (li << 4);
-                srec.push_back(r);
-                ++cnt;
-              }
-            }
-            scnt[(size_t)c * G + gg] = cnt;
-          }
-        }
-        for (int gg = G; gg <= 16; ++gg) h->sbase[gg] = (int)srec.size();
-        for (int z = 0; z < 16; ++z) {  // the ring reads up to two chunks past a stream's end
-          TermRec r;
-          memset(&r, 0, sizeof(r));
-          srec.push_back(r);
-        }
-        h->snchunk = NC;
-        e = cudaMalloc(&h->srec, srec.size() * sizeof(TermRec));
-        if (!e) e = cudaMemcpy(h->srec, srec.data(), srec.size() * sizeof(TermRec), cudaMemcpyHostToDevice);
-        if (!e) e = cudaMalloc(&h->smono, smono.size() * sizeof(unsigned long long));
-        if (!e) e = cudaMemcpy(h->smono, smono.data(), smono.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice);
-        if (!e) e = cudaMalloc(&h->schunk, chunks.size() * sizeof(uint4));
-        if (!e) e = cudaMemcpy(h->schunk, chunks.data(), chunks.size() * sizeof(uint4), cudaMemcpyHostToDevice);
-        if (!e) e = cudaMalloc(&h->scnt, scnt.size() * sizeof(unsigned));
-        if (!e) e = cudaMemcpy(h->scnt, scnt.data(), scnt.size() * sizeof(unsigned), cudaMemcpyHostToDevice);
-        if (e) {
-          cudaFree(h->srec);
-          cudaFree(h->smono);
-          cudaFree(h->schunk);
-          cudaFree(h->scnt);
-          h->srec = nullptr;
-          h->snchunk = 0;
-          e = cudaSuccess;
-        }
-      }
-    }
   }
   if (!e && T) e = cudaMemcpy(h->cs, d->coef_start, T * sizeof(cd), cudaMemcpyHostToDevice);
   if (!e && T) e = cudaMemcpy(h->ct, d->coef_target, T * sizeof(cd), cudaMemcpyHostToDevice);
@@ -602,64 +489,16 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   if (!e && T && d->param_slot) e = cudaMemcpy(h->pslot, d->param_slot, T, cudaMemcpyHostToDevice);
   if (e) {
     g_err = std::string("homotopy upload: ") + cudaGetErrorString(e);
-    delete h;
+    nid_homotopy_destroy(h);  // frees whatever was allocated (members start null)
     return 2;
   }
   *out = h;
   return 0;
 }
 
-int nid_homotopy_jit(NidHomotopy* h, const char* src, const char* include_dirs, char* log, int logcap) {
-  if (!h || !src) FAIL("null argument");
-  if (log && logcap > 0) log[0] = 0;
-  nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src, "nid_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) FAIL("nvrtcCreateProgram failed");
-  char name[64];
-  snprintf(name, sizeof(name), "track_ctl_kernel<%d, JitEval>", h->n);
-  nvrtcAddNameExpression(prog, name);
-  std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-default-device"};
-  if (include_dirs) {
-    std::string dirs(include_dirs);
-    size_t pos = 0;
-    while (pos <= dirs.size()) {
-      size_t e = dirs.find(':', pos);
-      if (e == std::string::npos) e = dirs.size();
-      if (e > pos) opts.push_back("-I" + dirs.substr(pos, e - pos));
-      pos = e + 1;
-    }
-  }
-  std::vector<const char*> copts;
-  for (auto& o : opts) copts.push_back(o.c_str());
-  nvrtcResult rc = nvrtcCompileProgram(prog, (int)copts.size(), copts.data());
-  size_t lsz = 0;
-  nvrtcGetProgramLogSize(prog, &lsz);
-  std::string lg(lsz, '\0');
-  if (lsz) nvrtcGetProgramLog(prog, &lg[0]);
-  if (log && logcap > 0) snprintf(log, (size_t)logcap, "%s", lg.c_str());
-  if (rc != NVRTC_SUCCESS) {
-    nvrtcDestroyProgram(&prog);
-    g_err = "NVRTC compile failed: " + lg.substr(0, 2000);
-    return 3;
-  }
-  const char* lowered = nullptr;
-  nvrtcGetLoweredName(prog, name, &lowered);
-  std::string lname = lowered ? lowered : "";
-  size_t csz = 0;
-  nvrtcGetCUBINSize(prog, &csz);
-  std::vector<char> cubin(csz);
-  nvrtcGetCUBIN(prog, cubin.data());
-  nvrtcDestroyProgram(&prog);
-  if (h->jit_lib) cudaLibraryUnload(h->jit_lib);
-  h->jit_lib = nullptr;
-  h->jit_kernel = nullptr;
-  CK(cudaLibraryLoadData(&h->jit_lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-  CK(cudaLibraryGetKernel(&h->jit_kernel, h->jit_lib, lname.c_str()));
-  return 0;
-}
-
 int nid_homotopy_destroy(NidHomotopy* h) {
   if (!h) return 0;
-  if (h->jit_lib) cudaLibraryUnload(h->jit_lib);
+  BIND();
   cudaFree(h->row_off);
   cudaFree(h->expo);
   delete h->ptab;
@@ -667,10 +506,6 @@ int nid_homotopy_destroy(NidHomotopy* h) {
   cudaFree(h->fex);
   if (h->rec) cudaFree(h->rec);
   if (h->runs) cudaFree(h->runs);
-  if (h->srec) cudaFree(h->srec);
-  if (h->smono) cudaFree(h->smono);
-  if (h->schunk) cudaFree(h->schunk);
-  if (h->scnt) cudaFree(h->scnt);
   cudaFree(h->cs);
   cudaFree(h->ct);
   cudaFree(h->acs);
@@ -731,6 +566,7 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
                       long long index_stride, const int32_t* degrees, const double* params, int param_div,
                       const double* path_texp, NidPathOut* out, int device_io, void* stream) {
   if (!h || !prm || !out) FAIL("null argument");
+  BIND();
   if (index_stride < 1) FAIL("index_stride must be >= 1");
   if (P < 0) FAIL("negative path count");
   const int n = h->n;
@@ -738,8 +574,7 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   memset(&g_counters, 0, sizeof(g_counters));
   if (P == 0) return 0;
   if (!starts && !degrees) FAIL("need explicit starts or total-degree degrees");
-  if (h->tw && (h->jit_kernel || h->rec))
-    FAIL("polyhedral homotopy: the JIT and streamed-record trackers do not evaluate t-weighted coefficients");
+  if (h->tw && h->rec) FAIL("polyhedral homotopy: the streamed-record tracker does not evaluate t-weighted coefficients");
   if (h->tw && !starts) FAIL("polyhedral homotopy: explicit (binomial) start points are required");
   if (h->nparam > 0 && !params) FAIL("homotopy has per-path parameters but none were given");
   if (param_div < 1) param_div = 1;
@@ -845,25 +680,13 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   a.gstate = ws<cd>(W_GSTATE, (size_t)max_blocks * 3 * n * rows::SLOTS);
   if (!a.gstate) FAIL("out of device memory (slot state)");
 
-  cudaEvent_t e0, e1, e2;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  CK(cudaEventCreate(&e2));
+  Events ev;
+  CK(cudaEventCreate(&ev.e[0]));
+  CK(cudaEventCreate(&ev.e[1]));
+  CK(cudaEventCreate(&ev.e[2]));
+  cudaEvent_t e0 = ev.e[0], e1 = ev.e[1], e2 = ev.e[2];
   CK(cudaEventRecord(e0, s));
-  if (h->jit_kernel) {
-    const void* fn = (const void*)h->jit_kernel;
-    const int threads = 32 * rows::groups_for(n);
-    const int smem = k_tsmem[n]();
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int per = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
-    if (per < 1) per = 1;
-    long long blocks = (long long)sm_count() * per;
-    const long long need = (P + 31) / 32;
-    if (need < blocks) blocks = need;
-    void* args[] = {(void*)&a};
-    CK(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, (size_t)smem, s));
-  } else if (h->ptab && !getenv("NID_NO_PTAB")) {
+  if (h->ptab && !getenv("NID_NO_PTAB")) {
     TrackArgsPT* pa = new TrackArgsPT;  // ~22 KB: off the stack
     pa->a = a;
     pa->t = *h->ptab;
@@ -907,14 +730,11 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   }
   unsigned long long hc[16];
   CK(cudaMemcpyAsync(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
-  for (int i = 0; i < 7; ++i) g_phase[i] = hc[8 + i];
   CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < 7; ++i) g_phase[i] = hc[8 + i];
   float ms1 = 0.f, ms2 = 0.f;
   cudaEventElapsedTime(&ms1, e0, e1);
   cudaEventElapsedTime(&ms2, e1, e2);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(e2);
   g_counters.evals = (long long)hc[0];
   g_counters.jacs = (long long)hc[1];
   g_counters.scales = (long long)hc[2];
@@ -929,6 +749,7 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
 int nid_eval_batch(NidHomotopy* h, int P, const double* x, const double* t, const double* params, int param_div,
                    double* H, double* J, double* scale) {
   if (!h || !x || !t || !H || !J || !scale) FAIL("null argument");
+  BIND();
   if (P <= 0) return 0;
   const int n = h->n;
   if (param_div < 1) param_div = 1;
@@ -967,6 +788,7 @@ int nid_eval_batch(NidHomotopy* h, int P, const double* x, const double* t, cons
 
 int nid_newton_step_batch(int n, int P, const double* J, const double* r, double* dx) {
   if (!J || !r || !dx) FAIL("null argument");
+  BIND();
   if (n < 1 || n > 16) FAIL("n must be in 1..16");
   if (P <= 0) return 0;
   cd* dJ = ws<cd>(W_J, (size_t)P * n * n);
@@ -991,6 +813,7 @@ int nid_newton_step_batch(int n, int P, const double* J, const double* r, double
 
 int nid_svd_batch(int m, int n, int P, const double* A, double* sv) {
   if (!A || !sv) FAIL("null argument");
+  BIND();
   if (n < 1 || n > 16 || m < n || m > 32) FAIL("need 1 <= n <= 16 and n <= m <= 32");
   if (P <= 0) return 0;
   cd* dA = ws<cd>(W_J, (size_t)P * m * n);
@@ -1008,6 +831,7 @@ int nid_refine_batch(NidHomotopy* h, int P, double* x, double tol, int iters, in
                      double infinity_threshold, double* residual, double* condition, int8_t* regular,
                      int32_t* rank, int8_t* slack_class) {
   if (!h || !x || !residual || !condition || !regular || !rank || !slack_class) FAIL("null argument");
+  BIND();
   if (h->nparam > 0) FAIL("refine does not take per-path parameters");
   if (P <= 0) return 0;
   const int n = h->n;
@@ -1048,6 +872,7 @@ int nid_refine_batch(NidHomotopy* h, int P, double* x, double tol, int iters, in
 
 int nid_dd_refine_batch(NidHomotopy* h, int P, double* x, int steps, int8_t* ok) {
   if (!h || !x || !ok) FAIL("null argument");
+  BIND();
   if (h->nparam > 0) FAIL("dd refine does not take per-path parameters");
   if (P <= 0) return 0;
   const int n = h->n;
@@ -1074,6 +899,7 @@ int nid_dd_refine_batch(NidHomotopy* h, int P, double* x, int steps, int8_t* ok)
 int nid_match_pairs(int n, int ncmp, int P, const double* X, int32_t* pairs, long long max_pairs,
                     long long* npairs) {
   if (!X || !npairs) FAIL("null argument");
+  BIND();
   if (ncmp < 1 || ncmp > n) FAIL("need 1 <= ncmp <= n");
   *npairs = 0;
   if (P <= 1) return 0;

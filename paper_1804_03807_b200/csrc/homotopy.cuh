@@ -62,18 +62,7 @@ struct HomDev {
   const TermRec* rec;
   const uint4* runs;
   int grun[17];
-  // shared monomials (track_sme.cuh) or null: chunk c = {degree, first
-  // monomial, monomials}, at most one per warp; group g's consumer records
-  // (coefficients x monomial slot) start at srec[sbase[g]], scnt[c * 8 + g]
-  // of them per chunk
-  const TermRec* srec;
-  const unsigned long long* smono;
-  const uint4* schunk;
-  const unsigned* scnt;
-  int snchunk;
-  int sbase[17];
 };
-constexpr int SME_KM = 4;  // widest shared monomial (total degree)
 
 NID_D cd ldg_c(const cd* p) {
   double2 v = __ldg(reinterpret_cast<const double2*>(p));

@@ -30,7 +30,6 @@
 #include "track_ptab.cuh"
 #include "track_rec.cuh"
 #include "track_rows.cuh"
-#include "track_sme.cuh"
 
 namespace ctl {
 
@@ -208,7 +207,7 @@ constexpr bool rec_on() {
   return N >= 8;
 }
 // dynamic shared memory of the table kernel: the slot layout, each warp's
-// ring of streamed term records, (n > 10) the shared-monomial exchange area;
+// ring of streamed term records;
 // the parameter-bank kernel needs the slot layout only
 template <int N>
 constexpr size_t ring_bytes() {
@@ -216,7 +215,7 @@ constexpr size_t ring_bytes() {
 }
 template <int N>
 constexpr size_t smem_bytes() {
-  return Lay<N>::bytes() + ring_bytes<N>() + (N > 10 ? sme::bytes() : 0);
+  return Lay<N>::bytes() + ring_bytes<N>();
 }
 
 // blocks per SM the register budget is sized for: as many as the shared
@@ -625,19 +624,14 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
 
 }  // namespace ctl
 
-// The default evaluator: the generic term-table interpreter (rows::eval_rows).
-// A JIT-compiled homotopy (csrc/jit_eval.h + paper_1804_03807_b200/jit.py)
-// supplies a policy with the same signature whose rows are straight-line code.
+// The table kernel's evaluator: the factor-list term-table interpreter
+// (rows::eval_rows_fac).
 template <int N>
 struct TableEval {
   static constexpr bool kTable = true;
   static NID_D void rows(const HomDev& H, int g, const cd (&x)[N], double t, const cd* prm, cd* aug, double* part,
                          bool want_scale, const cd* xs, double* axw) {
-#ifdef NID_EVAL_DENSE
-    rows::eval_rows<N>(H, g, x, t, prm, aug, part, want_scale);
-#else
     rows::eval_rows_fac<N>(H, g, xs, t, prm, aug, part, want_scale, axw);
-#endif
   }
   // per-cell polyhedral homotopy: tws = the slot's t-exponent row
   static NID_D void rows(const HomDev& H, int g, const cd (&x)[N], double t, const cd* prm, cd* aug, double* part,
@@ -739,18 +733,8 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
         const long long pr = lb[S + lane];
         const cd* prm = (act && pr >= 0) ? Ar.params + pr : nullptr;
         TermRec* ring = reinterpret_cast<TermRec*>(smem_ctl + L::bytes()) + g * 2 * rec::CHUNK;
-        bool sme_done = false;
-        if constexpr (N > 10) {
-          if (Ar.H.srec) {  // shared monomials (every warp of the block takes part)
-            eval_rows_sme<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
-                             db + L::AXW * S + lane, ring, smem_ctl + L::bytes() + ring_bytes<N>());
-            sme_done = true;
-          }
-        }
-        if (!sme_done) {
-          eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
-                           db + L::AXW * S + lane, ring);
-        }
+        eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+                         db + L::AXW * S + lane, ring);
         rec_done = true;
       }
     }

@@ -53,141 +53,6 @@ NID_D cd upow(cd x, int a) {
   return r;
 }
 
-// one term c x^a of the merged table: value into hv, partials into Jr; with
-// WS also the abs-sum contributions |c_s||x|^a, |c_t||x|^a (ax = |x_v|)
-template <int N, bool WS>
-NID_D void term(const HomDev& H, int k, const cd (&x)[N], const double (&ax)[N], double t, cd alpha, const cd* prm,
-                bool ml, cd& hv, cd (&Jr)[N], double& sS, double& sT) {
-  const uint4 ew = __ldg(H.expo + k);
-  const unsigned w[4] = {ew.x, ew.y, ew.z, ew.w};
-  cd ct = ldg_c(H.ct + k);
-  if (H.pslot != nullptr) {
-    const int s = __ldg(H.pslot + k);
-    if (s >= 0) ct = prm[s];
-  }
-  const cd c = H.td ? t * ct : alpha * ldg_c(H.cs + k) + t * ct;
-  cd P[N];
-  cd p = cd{1.0, 0.0};
-  double m = 1.0;
-  if (ml) {
-#pragma unroll
-    for (int v = 0; v < N; ++v) {
-      if (expo_at(w, v)) {  // warp-uniform
-        P[v] = p;
-        p = p * x[v];
-        if (WS) m = __dmul_rn(m, ax[v]);
-      }
-    }
-    hv = cfma(c, p, hv);
-    cd s = c;
-#pragma unroll
-    for (int v = N - 1; v >= 0; --v) {
-      if (expo_at(w, v)) {
-        Jr[v] = cfma(P[v], s, Jr[v]);
-        s = s * x[v];
-      }
-    }
-  } else {
-#pragma unroll
-    for (int v = 0; v < N; ++v) {
-      const int a = expo_at(w, v);
-      if (a) {
-        P[v] = p;
-        p = p * (a == 1 ? x[v] : upow(x[v], a));
-        if (WS) {
-          double pv = ax[v];
-#pragma unroll 1
-          for (int e = 1; e < a; ++e) pv = __dmul_rn(pv, ax[v]);
-          m = __dmul_rn(m, pv);
-        }
-      }
-    }
-    hv = cfma(c, p, hv);
-    cd s = c;
-#pragma unroll
-    for (int v = N - 1; v >= 0; --v) {
-      const int a = expo_at(w, v);
-      if (a == 1) {
-        Jr[v] = cfma(P[v], s, Jr[v]);
-        s = s * x[v];
-      } else if (a > 1) {
-        const cd q = upow(x[v], a - 1);
-        Jr[v] = cfma(P[v] * ((double)a * q), s, Jr[v]);
-        s = s * (q * x[v]);
-      }
-    }
-  }
-  if (WS) {
-    if (!H.td) sS = __dadd_rn(sS, __dmul_rn(__ldg(H.acs + k), m));
-    sT = __dadd_rn(sT, __dmul_rn(__ldg(H.act + k), m));
-  }
-}
-
-// The rows of warp group g (a host-balanced list) of H and J at (x, t) into
-// the slot's augmented matrix; partial max |H_i|^2 and abs-sum maxima into
-// the slot's double area.  The abs sums (noise scale, tracker.py:91-92) are
-// formed in the same pass whenever any lane of the warp needs them.
-template <int N>
-NID_D void eval_rows(const HomDev& H, int g, const cd (&x)[N], double t, const cd* prm, cd* aug, double* dbl,
-                     bool want_scale) {
-  using L = Layout<N>;
-  const cd alpha = (1.0 - t) * H.gamma;
-  const bool ml = H.multilinear != 0;
-  const bool ws = __any_sync(__activemask(), want_scale);
-  double ax[N];
-#pragma unroll
-  for (int v = 0; v < N; ++v) ax[v] = ws ? cabs_fast(x[v]) : 0.0;
-  double r2 = 0.0, mS = 0.0, mT = 0.0;
-#pragma unroll 1
-  for (int gi = H.goff[g]; gi < H.goff[g + 1]; ++gi) {
-    const int i = H.grow[gi];
-    cd hv = cd{0.0, 0.0};
-    cd Jr[N];
-#pragma unroll
-    for (int v = 0; v < N; ++v) Jr[v] = cd{0.0, 0.0};
-    const int k0 = __ldg(H.row_off + i), k1 = __ldg(H.row_off + i + 1);
-    double sS = 0.0, sT = 0.0;
-    if (ws) {
-#pragma unroll 1
-      for (int k = k0; k < k1; ++k) term<N, true>(H, k, x, ax, t, alpha, prm, ml, hv, Jr, sS, sT);
-    } else {
-#pragma unroll 1
-      for (int k = k0; k < k1; ++k) term<N, false>(H, k, x, ax, t, alpha, prm, ml, hv, Jr, sS, sT);
-    }
-    if (H.td) {  // G_i = x_i^{d_i} - 1 in closed form
-      const int d = H.tddeg[i];
-      const cd xi = pick<N>(x, i);
-      cd q = cd{1.0, 0.0};
-#pragma unroll 1
-      for (int e = 1; e < d; ++e) q = q * xi;
-      hv = cfma(alpha, q * xi - cd{1.0, 0.0}, hv);
-      const cd dj = alpha * ((double)d * q);
-#pragma unroll
-      for (int v = 0; v < N; ++v)
-        if (v == i) Jr[v] = Jr[v] + dj;
-      if (ws) {
-        double axi = 0.0;
-#pragma unroll
-        for (int v = 0; v < N; ++v)
-          if (v == i) axi = ax[v];
-        double m = 1.0;
-#pragma unroll 1
-        for (int e = 0; e < d; ++e) m = __dmul_rn(m, axi);
-        sS = __dadd_rn(1.0, m);  // |G_i| terms in the reference's order: constant, then x_i^d
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < N; ++v) A<N>(aug, i, v) = Jr[v];
-    A<N>(aug, i, N) = -hv;
-    r2 = nanmax(r2, cabs2(hv));
-    mS = fmax(mS, sS);
-    mT = fmax(mT, sT);
-  }
-  dbl[(L::R2 + g) * SLOTS] = r2;
-  dbl[(L::SS + g) * SLOTS] = mS;
-  dbl[(L::ST + g) * SLOTS] = mT;
-}
-
 // ---------------------------------------------------------------------------
 // Factor-list evaluator (the tracker's default): a term loops over the K
 // variables it contains (K = its factor count, dispatched to a fully
@@ -195,7 +60,7 @@ NID_D void eval_rows(const HomDev& H, int g, const cd (&x)[N], double t, const c
 // point is read from the slot's shared-memory copy and the Jacobian row is
 // accumulated in place in the augmented matrix.  The arithmetic -- prefix
 // products in ascending variable order, one suffix pass for the partials,
-// abs-sum scale -- is operation for operation that of `term` above.
+// abs-sum scale -- follows polynomials.py:236-256 (`_StackedEvaluator`).
 template <int N, int K, bool ML>
 NID_D void fterm(const HomDev& H, int k, const uint4 f, const cd* xs, const double* axs, bool ws, cd c, cd* row,
                  cd& hv, double& m) {

@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import weakref
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, fields
 
 import numpy as np
 
@@ -54,6 +54,15 @@ class TrackParams:
             int(self.max_corrector_iters), int(self.max_steps), self.infinity_threshold,
             self.endgame_start, self.endgame_contraction, self.snap_remaining,
             int(self.final_newton_iters), int(self.dd_refine_singular), self.soft_infinity, 0, 0)
+
+
+def params_c(params) -> _lib.TrackParamsC:
+    """The C-ABI struct of any TrackParams-shaped object: this package's
+    TrackParams, or the reference's own `nidpipe.tracker.TrackParams`
+    (tracker.py:109-134, same field names), re-validated here."""
+    if not isinstance(params, TrackParams):
+        params = TrackParams(**{f.name: getattr(params, f.name) for f in fields(TrackParams) if hasattr(params, f.name)})
+    return params.to_c()
 
 
 @dataclass(frozen=True)
@@ -159,26 +168,6 @@ class DeviceHomotopy:
     def n(self) -> int:
         return self.low.n
 
-    jit = False
-
-    def ensure_jit(self) -> None:
-        """Attach the NVRTC-specialised tracker (paper_1804_03807_b200/jit.py)."""
-        if not self.jit:
-            from . import jit as jitmod
-
-            jitmod.attach(self)
-
-
-# JIT heuristics: worth the ~4 s NVRTC compile for large launches of
-# moderately sized tables (huge tables make huge straight-line code)
-JIT_MIN_PATHS = 50_000
-JIT_MAX_TERMS = 1024
-
-
-def want_jit(dev: "DeviceHomotopy", paths: int, jit: bool | None) -> bool:
-    """The specialised kernel is opt-in: measured on C5 it removes the table
-    scaffolding but is not faster than the table kernel."""
-    return bool(jit)
 
 
 @dataclass(frozen=True)

@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .homotopy import DeviceHomotopy, Lowered, TrackParams, eval_batch
+from .homotopy import DeviceHomotopy, Lowered, TrackParams, eval_batch, params_c
 
 SLACK_MARGIN = 1e-9  # polyhedral.py:30
 
@@ -260,7 +260,7 @@ def track_cells(cells, g, supports, params: TrackParams = TrackParams()):
     o = _lib.PathOutC(_lib.ptr(out.x), _lib.ptr(out.status), _lib.ptr(out.steps), _lib.ptr(out.t_reached),
                       _lib.ptr(out.residual), _lib.ptr(out.condition), _lib.ptr(out.regular))
     L = _lib.lib()
-    pc = params.to_c()
+    pc = params_c(params)
     _lib.check(L.nid_track_cells(dev.handle, C.byref(pc), P, _lib.ptr(st), _lib.ptr(tw), C.byref(o), 0, None), L)
     out.counters = _lib.last_counters()
     return out, counts

@@ -13,12 +13,13 @@ the GPU replacement of `work_crew(jobs, p, lambda x0: track(h, x0, params))`
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
-from .homotopy import DeviceHomotopy, LinearHomotopy, TrackParams, lower, system_homotopy, want_jit  # noqa: F401
+from .homotopy import DeviceHomotopy, LinearHomotopy, TrackParams, lower, params_c, system_homotopy  # noqa: F401
 from .polys import PolySystem
 
 REGULAR = "regular"
@@ -110,10 +111,14 @@ def _device_of(h) -> DeviceHomotopy:
     if all(hasattr(h, a) for a in ("start", "target", "gamma")):
         # a reference nidpipe.tracker.LinearHomotopy (duck-typed: only
         # .start/.target/.gamma and .polys[i].terms are read)
-        cache = _FOREIGN.get(id(h))
-        if cache is None or cache[0] is not h:
-            cache = (h, LinearHomotopy(h.start, h.target, complex(h.gamma)))
-            _FOREIGN[id(h)] = cache
+        # cached per object without keeping it alive: the entry (and with it
+        # the uploaded device table) goes when the reference object does
+        key = id(h)
+        cache = _FOREIGN.get(key)
+        if cache is None or cache[0]() is not h:
+            cache = (weakref.ref(h), LinearHomotopy(h.start, h.target, complex(h.gamma)))
+            _FOREIGN[key] = cache
+            weakref.finalize(h, _FOREIGN.pop, key, None)
         return cache[1].device()
     raise TypeError("expected a LinearHomotopy or PolyhedralHomotopy (the GPU path tracks lowered homotopies)")
 
@@ -123,7 +128,7 @@ _FOREIGN: dict = {}
 
 def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=None, first_index: int = 0,
                 count: int | None = None, index_stride: int = 1, target_params=None, param_div: int = 1,
-                out: TrackResults | None = None, jit: bool | None = None) -> TrackResults:
+                out: TrackResults | None = None) -> TrackResults:
     """Track many paths of h in one launch.
 
     starts: [P, n] start points, or None with `degrees` for total-degree
@@ -145,15 +150,13 @@ def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=
         P = int(count)
         deg = np.ascontiguousarray(degrees, dtype=np.int32)
     prm = None if target_params is None else np.ascontiguousarray(target_params, dtype=np.complex128)
-    if want_jit(dev, P, jit):
-        dev.ensure_jit()
     if out is None:  # (callers may pass preallocated, e.g. pinned, host arrays)
         out = TrackResults(np.empty((P, n), np.complex128), np.empty(P, np.int8), np.empty(P, np.int32),
                            np.empty(P, np.float64), np.empty(P, np.float64), np.empty(P, np.float64),
                            np.empty(P, np.int8), {})
     o = _lib.PathOutC(_lib.ptr(out.x), _lib.ptr(out.status), _lib.ptr(out.steps), _lib.ptr(out.t_reached),
                       _lib.ptr(out.residual), _lib.ptr(out.condition), _lib.ptr(out.regular))
-    pc = params.to_c()
+    pc = params_c(params)
     _lib.check(L.nid_track_batch_strided(dev.handle, C.byref(pc), P, _lib.ptr(st), int(first_index),
                                          int(index_stride), _lib.ptr(deg), _lib.ptr(prm), int(param_div),
                                          C.byref(o), 0, None), L)
@@ -284,7 +287,7 @@ def classify(coords, n_original: int, infinity_threshold: float = 1e8, zero_tol:
 
 def track_batch_device(h, params: TrackParams, P: int, out: dict, *, degrees=None, first_index: int = 0,
                        index_stride: int = 1, starts_ptr: int = 0, params_ptr: int = 0, param_div: int = 1,
-                       stream: int = 0, jit: bool | None = None) -> dict:
+                       stream: int = 0) -> dict:
     """Device-resident variant of `track_batch`: every buffer is a device
     pointer (e.g. torch CUDA tensors' data_ptr()), nothing is copied, and the
     kernels run on `stream`.  `out` maps x_end/status/steps/t_reached/
@@ -292,12 +295,10 @@ def track_batch_device(h, params: TrackParams, P: int, out: dict, *, degrees=Non
     the path indices first_index + i * index_stride (a rank's strided shard)."""
     L = _lib.lib()
     dev = _device_of(h)
-    if want_jit(dev, P, jit):
-        dev.ensure_jit()
     deg = None if degrees is None else np.ascontiguousarray(degrees, dtype=np.int32)
     o = _lib.PathOutC(out["x_end"], out["status"], out["steps"], out["t_reached"], out["residual"],
                       out["condition"], out["regular"])
-    pc = params.to_c()
+    pc = params_c(params)
     _lib.check(L.nid_track_batch_strided(dev.handle, C.byref(pc), int(P), C.c_void_p(starts_ptr or None),
                                          int(first_index), int(index_stride), _lib.ptr(deg),
                                          C.c_void_p(params_ptr or None), int(param_div), C.byref(o), 1,

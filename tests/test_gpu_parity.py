@@ -215,23 +215,3 @@ def test_large_dense_quadrics_match_oracle(nid, n):
         if r.succeeded:
             x = r.endpoint.coordinates
             assert np.max(np.abs(res.x[i] - x)) / max(1.0, np.max(np.abs(x))) < 1e-8
-
-
-def test_shared_monomial_evaluator_matches_oracle(nid, monkeypatch):
-    """The opt-in shared-monomial evaluator (NID_SME=1, csrc/track_sme.cuh:
-    each distinct monomial formed once per slot and shared by every row) on a
-    13-variable dense quadric system: same statuses and endpoints as the
-    oracle."""
-    monkeypatch.setenv("NID_SME", "1")
-    n = 13
-    p = configs.total_degree_problem(f"Q{n}", configs.dense_quadrics(n, 100 + n), 100 + n)
-    idx = np.sort(np.random.default_rng(n + 1).choice(2 ** n, 16, replace=False))
-    starts = np.concatenate([systems.total_degree_starts(p.degrees, int(i), 1) for i in idx])
-    res = tracker.track_batch(gpu_h(p), starts)
-    h = O.LinearHomotopy(p.start, p.target, p.gamma)
-    for i in range(len(idx)):
-        r = O.track(h, starts[i])
-        assert (res.status[i] in (0, 2)) == r.succeeded, (i, res.status[i], r.status)
-        if r.succeeded:
-            x = r.endpoint.coordinates
-            assert np.max(np.abs(res.x[i] - x)) / max(1.0, np.max(np.abs(x))) < 1e-8

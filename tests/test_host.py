@@ -205,22 +205,3 @@ def test_two_rank_gloo_gather_and_reductions():
         assert p.exitcode == 0
     assert got == [0.0, 2.0, 3.0, 5.0, 6.0, 8.0, 9.0]  # indices with status 0 or 2, rank order
     assert mx == 1.0 and sm == 10
-
-
-def test_jit_generator_compiles_with_nvrtc():
-    """The specialised evaluator source (paper_1804_03807_b200/jit.py) for a
-    total-degree homotopy with exponent-2 terms and for a membership homotopy
-    with per-path coefficients compiles with NVRTC for sm_100a (no GPU needed)."""
-    from paper_1804_03807_b200 import jit
-    from paper_1804_03807_b200.filtering import WitnessSet
-    p = configs.c1()
-    src = jit.generate(lower(p.start, p.target, p.gamma))
-    assert "JitEval" in src and "0x" in src
-    jit.nvrtc_compile_check(src, 4)
-    pd = configs.c3_mini()
-    E = pd.emb.system
-    n, k = pd.emb.n_original, pd.emb.k
-    low = lower(E, E, 1.0, {(n + j, (0,) * E.nvars): j for j in range(k)})
-    src2 = jit.generate(low)
-    assert "prm[0]" in src2
-    jit.nvrtc_compile_check(src2, E.nvars)
