@@ -59,14 +59,14 @@ def test_c4_membership_matches_construction(c3_top):
     assert np.all((verdict == 1) == (labels == 1))
 
 
-def test_c4_hard_candidates_match_oracle(nid):
+def test_c4_hard_candidates_match_reference(nid):
     """The full 100,000-candidate C4 batch on a B200 disagreed with the
     construction labels on 4 candidates (3 on-component points reported off
-    it, 1 indeterminate).  The CPU oracle (the pinned restatement of
-    nidpipe.filtering.membership_test) reaches the same verdicts from the same
-    witness points (tests/golden/make_c4_hard.py): these are the reference's
-    answers, not GPU errors.  The GPU must reproduce the oracle exactly on
-    them and on six agreeing controls."""
+    it, 1 indeterminate).  The reference itself (nidpipe.filtering.
+    membership_test, filtering.py:92-127) reaches the same verdicts from the
+    same witness points (tests/golden/make_c4_hard.py): these are the
+    reference's answers, not GPU errors.  The GPU must reproduce nidpipe
+    exactly on them and on six agreeing controls."""
     from conftest import golden
     from paper_1804_03807_b200.tracker import Solution
 
@@ -75,4 +75,22 @@ def test_c4_hard_candidates_match_oracle(nid):
     pts = [Solution(w, 0.0, 1.0) for w in g["witness"]]
     W = filtering.WitnessSet(pd.emb.k, pd.emb, pts)
     verdict, _ = filtering.membership_batch(W, g["candidates"])
-    assert np.array_equal(verdict, g["oracle_verdict"]), (verdict, g["oracle_verdict"], g["labels"])
+    assert np.array_equal(verdict, g["reference_verdict"]), (verdict, g["reference_verdict"], g["labels"])
+
+
+def test_c4_membership_410_candidates_match_reference(nid):
+    """410 C4 candidates decided by nidpipe.filtering.membership_test itself
+    (tests/golden/make_fullsize.py gen_c4): 200 points on {h1 = h2 = 0} from
+    50 random 2-dim slices, 200 iid complex N(0,1) points, and the 10 hard
+    candidates above.  Every verdict (member / not a member / indeterminate)
+    must equal the reference's: classification is exact (north_star)."""
+    from conftest import golden
+    from paper_1804_03807_b200.tracker import Solution
+
+    g = golden("c4_membership_ref")
+    pd = configs.c3()
+    W = filtering.WitnessSet(pd.emb.k, pd.emb, [Solution(w, 0.0, 1.0) for w in g["witness"]])
+    verdict, tracked = filtering.membership_batch(W, g["candidates"])
+    bad = np.where(verdict != g["verdict"])[0]
+    assert bad.size == 0, (bad, verdict[bad], g["verdict"][bad], g["labels"][bad])
+    assert tracked <= 4 * len(g["candidates"])

@@ -152,3 +152,22 @@ def test_oracle_cascade_step_subset():
     ref = np.concatenate([g["L1_zero_x"], g["L1_nonzero_x"]])
     for s in nxt.zero_slack + nxt.nonzero_slack:
         assert np.min(np.max(np.abs(ref - s.coordinates), axis=1)) < 1e-8
+
+
+def test_oracle_membership_matches_reference_c4():
+    """The oracle's membership test on C4 candidates decided by nidpipe itself
+    (tests/golden/c4_hard.npz, c4_membership_ref.npz): the 10 hard
+    candidates (stored verdicts, both decided from the same witness points)
+    and two seeded candidates re-run here, one on the component and one off."""
+    from paper_1804_03807_b200 import configs
+
+    h = golden("c4_hard")
+    assert np.array_equal(h["oracle_verdict"], h["reference_verdict"])
+    g = golden("c4_membership_ref")
+    pd = configs.c3()
+    for i in (0, int(g["n_on"])):
+        try:
+            v = 1 if O.membership_test(list(g["witness"]), pd.emb, g["candidates"][i]) else 0
+        except O.MembershipIndeterminate:
+            v = -1
+        assert v == g["verdict"][i], (i, v, g["verdict"][i])
