@@ -34,8 +34,13 @@ if os.environ.get("NID_G10"):
     FLAGS = FLAGS + ["-DNID_G10=" + os.environ["NID_G10"]]
     OBJ = OBJ + "_G" + os.environ["NID_G10"]
 # experiment variants: extra -D flags, objects in their own directory
+# (NID_VARIANT_SIZES="10,...": only those sizes get the variant flags; the
+# other sizes link the default objects)
 EXTRA = os.environ.get("NID_EXTRA_DEFS", "").split()
+OBJ_DEFAULT = OBJ
+VARIANT_SIZES = [int(x) for x in os.environ.get("NID_VARIANT_SIZES", "").split(",") if x]
 if EXTRA:
+    FLAGS_DEFAULT = list(FLAGS)
     FLAGS = FLAGS + EXTRA
     OBJ = OBJ + "_" + "_".join(x.lstrip("-D").replace("=", "") for x in EXTRA)
 
@@ -67,10 +72,13 @@ def build(jobs: int | None = None, verbose: bool = False, force: bool = False, o
     cmds = []
     objs = []
     for n in sizes or SIZES:
-        o = os.path.join(OBJ, f"inst_{n}.o")
+        variant = not VARIANT_SIZES or n in VARIANT_SIZES
+        o = os.path.join(OBJ if variant else OBJ_DEFAULT, f"inst_{n}.o")
+        fl = FLAGS if variant or not EXTRA else FLAGS_DEFAULT
         objs.append(o)
         if force or _stale(o):
-            cmds.append([NVCC, *ARCH, *FLAGS, f"-DNID_N={n}", "-c", os.path.join(CSRC, "kernels_inst.cu"), "-o", o])
+            os.makedirs(os.path.dirname(o), exist_ok=True)
+            cmds.append([NVCC, *ARCH, *fl, f"-DNID_N={n}", "-c", os.path.join(CSRC, "kernels_inst.cu"), "-o", o])
     o = os.path.join(OBJ, "capi.o")
     objs.append(o)
     if force or _stale(o):
