@@ -678,6 +678,11 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   a.scratch = ws<cd>(W_SCR, (size_t)max_blocks * k_tthreads[n]() * (3 * n * n + 2 * n));
   if (!a.scratch) FAIL("out of device memory (scratch)");
   a.gstate = ws<cd>(W_GSTATE, (size_t)max_blocks * 3 * n * rows::SLOTS);
+  // per-slot evaluation of long paths (streamed-record tracker, n >= 8): in a
+  // small launch the slowest paths set the launch time, so a path switches
+  // after lat_steps steps; in a large one only far outliers do
+  a.lat_steps = P <= 16384 ? 64 : 512;
+  if (getenv("NID_LAT_STEPS")) a.lat_steps = atoi(getenv("NID_LAT_STEPS"));
   if (!a.gstate) FAIL("out of device memory (slot state)");
 
   Events ev;

@@ -53,7 +53,7 @@ enum IField {
   I_ACT, I_MODE, I_CTX, I_CITERS, I_CIT, I_CPHASE, I_CITS, I_DNIT, I_DNTRIAL, I_USED, I_OUTST, I_FLAGS, I_BAD,
   I_COUNT
 };
-enum Flag { F_COK = 1, F_HAVEPREV = 2, F_ENDGAME = 4, F_NEEDSCALE = 8, F_HASX = 16, F_FALLBACK = 32 };
+enum Flag { F_COK = 1, F_HAVEPREV = 2, F_ENDGAME = 4, F_NEEDSCALE = 8, F_HASX = 16, F_FALLBACK = 32, F_LAT = 64 };
 
 template <int N>
 struct Lay {
@@ -207,15 +207,26 @@ constexpr bool rec_on() {
   return N >= 8;
 }
 // dynamic shared memory of the table kernel: the slot layout, each warp's
-// ring of streamed term records;
+// ring of streamed term records and per-slot evaluation scratch;
 // the parameter-bank kernel needs the slot layout only
 template <int N>
 constexpr size_t ring_bytes() {
   return rec_on<N>() ? (size_t)rows::groups<N>() * 2 * rec::CHUNK * sizeof(TermRec) : 0;
 }
+// per-slot evaluation of long paths, where its scratch fits beside the slot
+// layout and the rings (n = 8 .. 14; not n = 15, 16)
+template <int N>
+constexpr bool lat_on() {
+  return rec_on<N>() && Lay<N>::bytes() + ring_bytes<N>() + (size_t)rows::groups<N>() * lat::warp_bytes<N>() +
+                            1024 <= (size_t)227 * 1024;
+}
+template <int N>
+constexpr size_t lat_bytes() {
+  return lat_on<N>() ? (size_t)rows::groups<N>() * lat::warp_bytes<N>() : 0;
+}
 template <int N>
 constexpr size_t smem_bytes() {
-  return Lay<N>::bytes() + ring_bytes<N>();
+  return Lay<N>::bytes() + ring_bytes<N>() + lat_bytes<N>();
 }
 
 // blocks per SM the register budget is sized for: as many as the shared
@@ -509,6 +520,7 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
           continue;
         }
         IS_(I_USED) += 1;
+        if (IS_(I_USED) > Ar.lat_steps) SETF(F_LAT, true);  // per-slot evaluation from now on
         double hs = fmin(fmin(DS_(D_STEP), q.max_step), rem);
         if (HAS(F_ENDGAME)) hs = fmin(hs, q.endgame_contraction * rem);
         double tt = t + hs;
@@ -728,13 +740,28 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     bool rec_done = false;
     if constexpr (rec_on<N>() && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value) {
       if (Ar.H.rec) {  // streamed records: every lane of the warp takes part
-        const bool act = W_IS(I_ACT) == A_EVAL;
+        const bool act0 = W_IS(I_ACT) == A_EVAL;
+        const bool lat = lat_on<N>() && act0 && (W_IS(I_FLAGS) & F_LAT) != 0;
+        const bool act = act0 && !lat;  // slots of the row-per-warp pass
         const bool want = act && (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
         const long long pr = lb[S + lane];
         const cd* prm = (act && pr >= 0) ? Ar.params + pr : nullptr;
         TermRec* ring = reinterpret_cast<TermRec*>(smem_ctl + L::bytes()) + g * 2 * rec::CHUNK;
-        eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
-                         db + L::AXW * S + lane, ring);
+        if (__any_sync(0xffffffffu, act))
+          eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+                           db + L::AXW * S + lane, ring);
+        // paths past lat_steps steps: one slot at a time, the warp's lanes split the terms
+        unsigned lm = __ballot_sync(0xffffffffu, lat);
+        unsigned char* scr = smem_ctl + L::bytes() + ring_bytes<N>() + (size_t)g * lat::warp_bytes<N>();
+#pragma unroll 1
+        while (lat_on<N>() && lm) {
+          const int s = __ffs(lm) - 1;
+          lm &= lm - 1;
+          const long long ps = lb[S + s];
+          const bool ws = (ib[I_FLAGS * S + s] & (F_NEEDSCALE | F_FALLBACK)) != 0;
+          eval_slot_rec<N>(Ar.H, g, cb + L::XE * S + s, db[D_TE * S + s], (Ar.params && ps >= 0) ? Ar.params + ps : nullptr,
+                           cb + s, db + L::PART * S + s, ws, db + L::AXW * S + s, scr);
+        }
         rec_done = true;
       }
     }

@@ -265,3 +265,200 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
     dbl[(L::ST + g) * S] = mT;
   }
 }
+
+// ---------------------------------------------------------------------------
+// Per-slot ("latency") evaluation of the streamed records.  The row-per-warp
+// evaluator above serves 32 slots per pass, one term at a time per lane: a
+// block iteration lasts as long as a warp's walk over its rows' terms (~500
+// for C3's heavy rows) whether 32 slots are active or one.  In the tail of a
+// small launch (a cascade level of ~5k paths whose slowest path takes 30x the
+// mean number of steps) almost every slot is idle, so a path that has taken
+// more than TrackArgs::lat_steps steps is evaluated here instead: the warp's
+// 32 lanes split its rows' terms (lane l takes records l, l+32, ...), each
+// lane accumulates into its own row of a per-warp shared-memory scratch, and
+// the rows are summed in lane order.  The term arithmetic is t_load /
+// t_compute / t_commit's; only the summation order differs, and the switch is
+// a function of the path's own step count, so results stay deterministic.
+namespace lat {
+
+// per-warp scratch: the slot's point and moduli, then 32 lane rows of NP
+// complex (J_v for v < N, H at N, the two abs sums at N+1; NP odd so lane
+// rows start in different banks)
+template <int N>
+constexpr int NP() {
+  return (N + 2) | 1;
+}
+template <int N>
+constexpr size_t warp_bytes() {  // xb[N] cd, 32 lane rows of NP cd, axb[N] double; 16-byte multiple
+  return ((size_t)N * sizeof(cd) + (size_t)32 * NP<N>() * sizeof(cd) + (size_t)N * sizeof(double) + 15) & ~(size_t)15;
+}
+
+template <int N, int K>
+NID_D void lane_terms(const TermRec* recs, long long r, long long r1, const cd* xb, const double* axb, bool ws,
+                      bool td, cd alpha, double t, const cd* prm, cd* jl, cd& hv, double& sS, double& sT) {
+  TermRec Rn;
+  if (r < r1) Rn = recs[r];
+#pragma unroll 1
+  for (; r < r1; r += 32) {
+    const TermRec R = Rn;
+    if (r + 32 < r1) Rn = recs[r + 32];  // the next record's L2 trip overlaps this term
+    rec::TermState<(K > 0 ? K : 1)> S;
+    cd ct = cd{R.ctr, R.cti};
+    if (prm && R.pslot >= 0) ct = prm[R.pslot];
+    const cd c = td ? t * ct : alpha * cd{R.csr, R.csi} + t * ct;
+    if (K == 0) {
+      hv = hv + c;
+      if (ws) {
+        if (!td) sS = __dadd_rn(sS, R.acs);
+        sT = __dadd_rn(sT, R.act);
+      }
+      continue;
+    }
+    const unsigned long long meta = R.meta;
+    S.p = c;
+    S.dup = (unsigned)(meta >> 52) & ~1u;
+    S.acs = R.acs;
+    S.act = R.act;
+    S.m = 1.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) S.v[j] = (int)((meta >> (4 * j)) & 15);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      S.Jv[j] = jl[S.v[j]];
+      S.X[j] = xb[S.v[j]];
+      if (ws) S.m = __dmul_rn(S.m, axb[S.v[j]]);
+    }
+    rec::t_compute<(K > 0 ? K : 1)>(S);
+    // t_commit on the lane's row (stride 1 instead of SLOTS)
+    hv = hv + S.p;
+    if (K > 1 && S.dup) {
+#pragma unroll
+      for (int j = K - 1; j > 0; --j)
+        if (S.dup & (1u << j)) S.d[j - 1] = S.d[j - 1] + S.d[j];
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (!(S.dup & (1u << j))) jl[S.v[j]] = S.Jv[j] + S.d[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < K; ++j) jl[S.v[j]] = S.Jv[j] + S.d[j];
+    }
+    if (ws) {
+      if (!td) sS = __dadd_rn(sS, __dmul_rn(S.acs, S.m));
+      sT = __dadd_rn(sT, __dmul_rn(S.act, S.m));
+    }
+  }
+}
+
+}  // namespace lat
+
+// The rows of warp group g for ONE slot s (warp-uniform), every lane taking
+// part.  xs / axs / aug / dbl: the block's arrays at slot s (stride SLOTS);
+// scr: this warp's lat::warp_bytes<N>() of shared memory.
+template <int N>
+NID_D void eval_slot_rec(const HomDev& H, int g, const cd* xs, double t, const cd* prm, cd* aug, double* dbl, bool ws,
+                         const double* axs, unsigned char* scr) {
+  using L = rows::Layout<N>;
+  constexpr int S = rows::SLOTS;
+  constexpr int NP = lat::NP<N>();
+  const int lane = threadIdx.x & 31;
+  cd* const xb = reinterpret_cast<cd*>(scr);
+  cd* const rowsl = xb + N;  // 32 lane rows of NP
+  double* const axb = reinterpret_cast<double*>(rowsl + 32 * NP);
+  cd* const jl = rowsl + lane * NP;
+  __syncwarp();  // the previous slot's readers are done with the scratch
+  if (lane < N) {
+    xb[lane] = xs[lane * S];
+    axb[lane] = ws ? axs[lane * S] : 0.0;
+  }
+  const cd alpha = (1.0 - t) * H.gamma;
+  const bool td = H.td != 0;
+  double r2 = 0.0, mS = 0.0, mT = 0.0;
+  const int u0 = H.grun[g], u1 = H.grun[g + 1];
+  int row_i = -1;
+  cd hv = cd{0.0, 0.0};
+  double sS = 0.0, sT = 0.0;
+#pragma unroll
+  for (int v = 0; v < N; ++v) jl[v] = cd{0.0, 0.0};
+  __syncwarp();
+#pragma unroll 1
+  for (int u = u0; u <= u1; ++u) {
+    const uint4 run = u < u1 ? __ldg(&H.runs[u]) : make_uint4(0xffffffffu, 0u, 0u, 0u);
+    if ((int)run.x != row_i) {
+      if (row_i >= 0) {  // close the row: sum the lane rows in lane order
+        jl[N] = hv;
+        jl[N + 1] = cd{sS, sT};
+        __syncwarp();
+        if (lane <= N + 1) {
+          cd acc = rowsl[lane];
+#pragma unroll 4
+          for (int l = 1; l < 32; ++l) acc = acc + rowsl[l * NP + lane];
+          if (lane < N) {
+            if (td && lane == row_i) {  // start system G_i = x_i^{d_i} - 1, Jacobian term
+              const int d = H.tddeg[row_i];
+              const cd xi = xb[row_i];
+              cd q = cd{1.0, 0.0};
+#pragma unroll 1
+              for (int e = 1; e < d; ++e) q = q * xi;
+              acc = acc + alpha * ((double)d * q);
+            }
+            aug[(row_i * (N + 1) + lane) * S] = acc;
+          } else if (lane == N) {
+            cd h = acc;
+            if (td) {
+              const int d = H.tddeg[row_i];
+              const cd xi = xb[row_i];
+              cd q = cd{1.0, 0.0};
+#pragma unroll 1
+              for (int e = 1; e < d; ++e) q = q * xi;
+              h = cfma(alpha, q * xi - cd{1.0, 0.0}, h);
+            }
+            aug[(row_i * (N + 1) + N) * S] = -h;
+            r2 = nanmax(r2, cabs2(h));
+          } else {  // lane N + 1: the abs sums
+            double s0 = acc.re;
+            if (td && ws) {
+              const double axi = axb[row_i];
+              double m = 1.0;
+#pragma unroll 1
+              for (int e = 0; e < H.tddeg[row_i]; ++e) m = __dmul_rn(m, axi);
+              s0 = __dadd_rn(1.0, m);
+            }
+            mS = fmax(mS, s0);
+            mT = fmax(mT, acc.im);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < N; ++v) jl[v] = cd{0.0, 0.0};
+        hv = cd{0.0, 0.0};
+        sS = 0.0;
+        sT = 0.0;
+        __syncwarp();
+      }
+      if (u == u1) break;
+      row_i = (int)run.x;
+    }
+    const int K = (int)run.y;
+    const long long r0 = (long long)run.z + lane, r1 = (long long)run.z + run.w;
+    switch (K) {
+#define NID_LT(KK)                                                                                          \
+  case KK:                                                                                                  \
+    lat::lane_terms<N, KK>(H.rec, r0, r1, xb, axb, ws, td, alpha, t, prm, jl, hv, sS, sT);                \
+    break;
+      NID_LT(0) NID_LT(1) NID_LT(2) NID_LT(3) NID_LT(4) NID_LT(5) NID_LT(6) NID_LT(7) NID_LT(8)
+      NID_LT(9) NID_LT(10) NID_LT(11) NID_LT(12)
+#undef NID_LT
+      default:
+        break;
+    }
+  }
+  // partial maxima of this warp's rows for the slot (lanes N and N+1 hold them)
+  r2 = __shfl_sync(0xffffffffu, r2, N);
+  mS = __shfl_sync(0xffffffffu, mS, N + 1);
+  mT = __shfl_sync(0xffffffffu, mT, N + 1);
+  if (lane == 0) {
+    dbl[(L::R2 + g) * S] = r2;
+    dbl[(L::SS + g) * S] = mS;
+    dbl[(L::ST + g) * S] = mT;
+  }
+}

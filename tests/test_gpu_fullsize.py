@@ -1,0 +1,137 @@
+"""Full-size parity against fixtures decided by the REFERENCE itself
+(tests/golden/make_fullsize.py runs nidpipe on this framework's seeded
+inputs): a 2,048-path sample of the C3 top continuation with the
+reference's own level classification, a chain of reference cascade_step
+calls d = 6 .. 1 (each from the reference's own nonzero-slack solutions of
+the level above), and a seeded uniform sample of C5 paths.
+
+Exact: finite-path sets, per-level counts (starts / at infinity / zero slack
+/ nonzero slack / failures), except that a point whose refined slack sits on
+the 1e-8 zero-slack threshold (within 10x) may land on either side.  Within
+1e-8 relative: finite endpoints path by path, nonzero-slack solutions as
+sets.  Zero-slack points below the top
+dimension lie on the 6-dimensional component (junk for that level), so where
+a path lands on it depends on rounding history: their count is exact, their
+coordinates are not compared.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_1804_03807_b200 import cascade, configs, systems, tracker
+from paper_1804_03807_b200.homotopy import LinearHomotopy, TrackParams
+from paper_1804_03807_b200.tracker import Solution
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_rows(a, b):
+    return np.max(np.abs(a - b), axis=-1) / np.maximum(1.0, np.max(np.abs(b), axis=-1))
+
+
+def assert_sets_match(gpu_x, ref_x, tol=1e-8):
+    """Every GPU point has a reference point within tol and vice versa."""
+    assert len(gpu_x) == len(ref_x)
+    if len(ref_x) == 0:
+        return
+    d = np.max(np.abs(gpu_x[:, None, :] - ref_x[None, :, :]), axis=2) / np.maximum(
+        1.0, np.max(np.abs(ref_x), axis=1))[None, :]
+    assert d.min(axis=1).max() < tol, d.min(axis=1).max()
+    assert d.min(axis=0).max() < tol, d.min(axis=0).max()
+
+
+def counts_of(lv):
+    return [lv.starts, lv.at_infinity, len(lv.zero_slack), len(lv.nonzero_slack), lv.failures]
+
+
+@pytest.fixture(scope="module")
+def chain():
+    return golden("c3_cascade_chain")
+
+
+def test_c3_top_sample_2048_matches_reference(nid, chain):
+    """2,048 seeded C3 top paths (n = 14): the finite set equals the
+    reference's path by path, endpoints within 1e-8, and the reference's
+    _classify_level counts (cascade.py:249-277) are reproduced exactly."""
+    pd = configs.c3()
+    h, _ = cascade.top_homotopy(pd.emb)
+    res = tracker.track_batch(h, chain["top_starts"])
+    st_ref = chain["top_status"].astype(int)
+    fin_g, fin_r = res.succeeded, np.isin(st_ref, (0, 2))
+    assert np.array_equal(fin_g, fin_r), (np.where(fin_g != fin_r)[0], res.status[fin_g != fin_r])
+    assert np.mean(res.status == st_ref) >= 0.99
+    assert np.all(rel_rows(res.x[fin_g], chain["top_x"][fin_r]) < 1e-8)
+    lv = cascade._classify_level(res, pd.emb, pd.emb.k, TrackParams())
+    assert counts_of(lv) == chain["top_counts"].tolist()
+    assert_sets_match(np.array([s.coordinates for s in lv.nonzero_slack]).reshape(-1, 14), chain["top_nonzero_x"])
+
+
+def nearest(A, B):
+    """For every row of A, the relative distance to the nearest row of B."""
+    if len(A) == 0:
+        return np.zeros(0)
+    if len(B) == 0:
+        return np.full(len(A), np.inf)
+    d = np.max(np.abs(A[:, None, :] - B[None, :, :]), axis=2) / np.maximum(1.0, np.max(np.abs(B), axis=1))[None, :]
+    return d.min(axis=1)
+
+
+BORDER = 1e-7  # zero-slack test is max|slack| < 1e-8 (tracker.py:45): 10x band
+
+
+@pytest.mark.parametrize("d", [6, 5, 4, 3, 2, 1])
+def test_c3_cascade_step_matches_reference(nid, chain, d):
+    """cascade_step at dimension d (cascade.py:296-322) from the reference's
+    own nonzero-slack solutions.  Starts, at-infinity and failure counts are
+    exact, and so is zero + nonzero.  The zero/nonzero split is exact except
+    for points on the 1e-8 slack threshold: every reference nonzero-slack
+    solution either matches a GPU nonzero-slack solution within 1e-8 or has
+    max|slack| < 1e-7 (and then the GPU called it zero-slack), and vice
+    versa.  Such a point is a junk point on the 6-dimensional component whose
+    slack after refinement is rounding noise around 1e-8 (d = 2: one point,
+    reference slack 1.7e-8, GPU 7e-12, condition 1e14)."""
+    pd = configs.c3()
+    emb = pd.emb.level(d)
+    sols = [Solution(x, float(r), float(c)) for x, r, c in zip(chain[f"in{d}_x"], chain[f"in{d}_res"],
+                                                                chain[f"in{d}_cond"])]
+    level = cascade.CascadeLevel(d, emb, starts=len(sols), at_infinity=0, nonzero_slack=sols)
+    nxt = cascade.cascade_step(level)
+    got, ref = counts_of(nxt), chain[f"out{d}_counts"].tolist()
+    assert (got[0], got[1], got[4]) == (ref[0], ref[1], ref[4]), (got, ref)
+    assert got[2] + got[3] == ref[2] + ref[3], (got, ref)
+    n0 = pd.emb.n_original
+    nv = n0 + d - 1
+    g_nz = np.array([s.coordinates for s in nxt.nonzero_slack]).reshape(-1, nv)
+    r_nz = chain[f"out{d}_nonzero_x"]
+    r_only = nearest(r_nz, g_nz) >= 1e-8
+    g_only = nearest(g_nz, r_nz) >= 1e-8
+    for pts in (r_nz[r_only], g_nz[g_only]):
+        if len(pts):
+            assert pts.shape[1] > n0 and np.all(np.max(np.abs(pts[:, n0:]), axis=1) < BORDER), pts[:, n0:]
+    assert got[3] - ref[3] == int(g_only.sum()) - int(r_only.sum())
+    assert int(r_only.sum()) + int(g_only.sum()) <= max(1, len(r_nz) // 100)
+    for s in nxt.zero_slack:
+        assert np.max(np.abs(s.coordinates[n0:])) < 1e-8 if s.coordinates.size > n0 else True
+
+
+def test_c5_full_sample_matches_reference(nid):
+    """A seeded uniform sample of C5 paths tracked by nidpipe itself
+    (make_fullsize.py gen_c5, >= 131,072 paths): the finite set equals the
+    reference's path by path (so the finite count is exact), the endpoints
+    of finite paths match within 1e-8, statuses agree on >= 97 % (the
+    at_infinity / failed split of slowly diverging paths is rounding
+    sensitive)."""
+    p = configs.c5()
+    fix = golden("track_c5_full_sample")
+    idx = fix["index"]
+    assert len(idx) >= 131072
+    h = LinearHomotopy(p.start, p.target, p.gamma)
+    starts = systems.total_degree_starts_at(p.degrees, idx)
+    res = tracker.track_batch(h, starts)
+    st_g, st_r = res.status.astype(int), fix["status"].astype(int)
+    fin_g, fin_r = np.isin(st_g, (0, 2)), np.isin(st_r, (0, 2))
+    diff = np.where(fin_g != fin_r)[0]
+    assert diff.size == 0, (diff, st_g[diff], st_r[diff])
+    assert np.mean(st_g == st_r) >= 0.97
+    assert np.all(rel_rows(res.x[fin_g], fix["fin_x"]) < 1e-8)
