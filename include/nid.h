@@ -21,6 +21,7 @@
  *                         _endpoint_solution / _dd_polish              tracker.py:255-302
  *   nid_track_batch_strided  the same over a rank's strided share of the
  *                         start-path indices (one process per GPU)     parallel.py:69-109
+ *   nid_track_trace       track(h, x0, params, trace=list)              tracker.py:341-407
  *   nid_track_cells       solve_start_system's per-cell solve_cell loop cascade.py:134-141,
  *                         (cells batched, one t-exponent row per path) polyhedral.py:794-811
  *   nid_refine_batch      newton_refine + classify                     tracker.py:410-455
@@ -52,7 +53,10 @@ extern "C" {
 #define NID_CLS_ZERO_SLACK 4
 #define NID_CLS_NONZERO_SLACK 5
 
-/* The TrackParams fields (tracker.py:113-127); precision: 0 double. */
+/* The TrackParams fields (tracker.py:113-127); precision: 0 double,
+ * 1 double_double (every H / J evaluation in complex double-double rounded
+ * to double, no evaluation-noise floor, every endpoint polished:
+ * _DDView / _track_dd, tracker.py:458-497). */
 typedef struct NidTrackParams {
   double initial_step, min_step, max_step, corrector_tol;
   int32_t max_corrector_iters, max_steps;
@@ -157,6 +161,15 @@ int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, co
                             long long first_index, long long index_stride, const int32_t* degrees,
                             const double* params, int param_div, NidPathOut* out, int device_io,
                             void* stream);
+
+/* track(h, x0, params, trace=list) (tracker.py:341-407): nid_track_batch on
+ * host buffers that also records, per path, the (t, step, corrector
+ * iterations) triple of every accepted step (tracker.py:393-394):
+ * trace[(p * trace_cap + k) * 3 .. +3) for k < min(trace_n[p], trace_cap);
+ * trace_n[p] is the path's accepted-step count (it may exceed trace_cap:
+ * max_steps is always enough). */
+int nid_track_trace(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, const double* params,
+                    int param_div, NidPathOut* out, int trace_cap, double* trace, int32_t* trace_n);
 
 int nid_last_counters(NidCounters* c);
 

@@ -22,7 +22,7 @@ EXPORTS = (
     "nid_last_error", "nid_device_count", "nid_init", "nid_shutdown", "nid_homotopy_create",
     "nid_homotopy_destroy", "nid_eval_batch", "nid_newton_step_batch", "nid_svd_batch",
     "nid_track_batch", "nid_track_batch_strided", "nid_last_counters", "nid_refine_batch", "nid_dd_refine_batch",
-    "nid_match_pairs", "nid_track_cells",
+    "nid_match_pairs", "nid_track_cells", "nid_track_trace",
 )
 
 
@@ -94,6 +94,7 @@ def load_library():
             "nid_track_batch": ([p, p, i, p, ll, p, p, i, p, i, p], i),
             "nid_track_batch_strided": ([p, p, i, p, ll, ll, p, p, i, p, i, p], i),
             "nid_track_cells": ([p, p, i, p, p, p, i, p], i),
+            "nid_track_trace": ([p, p, i, p, p, i, p, i, p, p], i),
             "nid_last_counters": ([p], i),
             "nid_refine_batch": ([p, i, p, d, i, i, d, p, p, p, p, p], i),
             "nid_dd_refine_batch": ([p, i, p, i, p], i),

@@ -16,38 +16,18 @@ returning the fields of the reference's `DecompositionReport`
 from __future__ import annotations
 
 import time
-from dataclasses import dataclass, field
-
 from . import polyhedral as ph
 from .cascade import TopStats, run_cascade, solve_top
 from .filtering import classify_isolated, filter_junk
+from . import refbridge
 from .homotopy import TrackParams
+from .report import DecompositionReport, Timings
 from .systems import embed
 
 
-@dataclass
-class Decomposition:
-    """The DecompositionReport fields (report.py:51-70)."""
-
-    seed: int
-    top_dimension: int
-    tasks: int
-    precision: str
-    nvars: int
-    names: tuple
-    witness_sets: list
-    isolated: list
-    suspects: list
-    cascade_counts: list
-    filter_stages: list
-    top_stats: TopStats
-    timings: dict = field(default_factory=dict)
-    warnings: list = field(default_factory=list)
-    superset: object = None  # the cascade's WitnessSuperset (not in the reference's report)
-
-    @property
-    def degrees(self) -> dict:
-        return {w.dimension: w.degree for w in self.witness_sets}
+# the record decompose returns: the reference's DecompositionReport fields
+# (report.py:51-70) plus the cascade's WitnessSuperset
+Decomposition = DecompositionReport
 
 
 def enumerate_cells_host(system, seed: int) -> list:
@@ -71,11 +51,13 @@ def enumerate_cells_host(system, seed: int) -> list:
 
 
 def decompose(f, top_dimension: int | None = None, seed: int = 0, tasks: int = 1, precision: str = "double",
-              mode: str = "gpu", cell_log: list | None = None, cells=None) -> Decomposition:
+              mode: str = "gpu", cell_log: list | None = None, cells=None,
+              input_path: str | None = None) -> DecompositionReport:
     """Numerical irreducible decomposition with every path on the GPU
-    (blackbox.py:36-110)."""
-    if mode != "gpu":
-        raise ValueError(f"unknown mode {mode!r}: this package tracks on the GPU")
+    (blackbox.py:36-110).  mode "thread" / "process" is the reference's CPU
+    work crew: delegated to nidpipe.blackbox.decompose when it is importable."""
+    if not refbridge.check_mode(mode):
+        return refbridge.decompose(f, top_dimension, seed, tasks, precision, mode, cell_log)
     if len(f.polys) != f.nvars:
         raise ValueError("give a square system (square_up stays with the reference)")
     warnings: list = []
@@ -86,26 +68,26 @@ def decompose(f, top_dimension: int | None = None, seed: int = 0, tasks: int = 1
                         "(an overestimate causes significant extra work)")
     if not 0 <= top_dimension < n:
         raise ValueError(f"top dimension must be in 0..{n - 1}, got {top_dimension}")
-    if precision != "double":
-        raise ValueError("only precision='double' tracks on the GPU (double-double tracking is not built)")
-    params = TrackParams()
-    timings: dict = {}
+    if precision not in ("double", "dd"):
+        raise ValueError(f"unknown precision {precision!r}")
+    params = TrackParams(precision="double_double" if precision == "dd" else "double")
+    timings = Timings()
     emb = embed(f, top_dimension, seed)
     system = emb.system if emb.k > 0 else emb.base
     t0 = time.perf_counter()
     if cells is None:
         cells = enumerate_cells_host(system, seed)
-    timings["cells"] = time.perf_counter() - t0
+    timings.cells = time.perf_counter() - t0
     top_results, top_stats = solve_top(emb, tasks, seed, params, mode, cell_log, cells=cells)
-    timings["start_system"] = top_stats.time_start_system
-    timings["continuation"] = top_stats.time_continuation
+    timings.start_system = top_stats.time_start_system + timings.cells
+    timings.continuation = top_stats.time_continuation
     t0 = time.perf_counter()
     superset = run_cascade(top_results, emb, tasks, params, mode)
-    timings["cascade"] = time.perf_counter() - t0
+    timings.cascade = time.perf_counter() - t0
     t0 = time.perf_counter()
     witness_sets, stages = filter_junk(superset, tasks, params, mode)
     isolated, suspects, iso_stages = classify_isolated(superset.candidates(0), witness_sets, f, tasks, params, mode)
-    timings["filtering"] = time.perf_counter() - t0
-    return Decomposition(seed, top_dimension, tasks, precision, n, tuple(getattr(f, "names", ()) or ()),
-                         witness_sets, isolated, suspects, [lv.counts for lv in superset.levels],
-                         stages + iso_stages, top_stats, timings, warnings, superset)
+    timings.filtering = time.perf_counter() - t0
+    return DecompositionReport(seed, top_dimension, tasks, precision, n, tuple(getattr(f, "names", ()) or ()),
+                               witness_sets, isolated, suspects, [lv.counts for lv in superset.levels],
+                               stages + iso_stages, top_stats, timings, input_path, warnings, superset)

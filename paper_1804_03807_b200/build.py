@@ -79,6 +79,14 @@ def build(jobs: int | None = None, verbose: bool = False, force: bool = False, o
         if force or _stale(o):
             os.makedirs(os.path.dirname(o), exist_ok=True)
             cmds.append([NVCC, *ARCH, *fl, f"-DNID_N={n}", "-c", os.path.join(CSRC, "kernels_inst.cu"), "-o", o])
+    # the auxiliary tracker kernel (double-double tracking, step traces): always default flags
+    for n in sizes or SIZES:
+        o = os.path.join(OBJ_DEFAULT, f"aux_{n}.o")
+        objs.append(o)
+        if force or _stale(o):
+            os.makedirs(os.path.dirname(o), exist_ok=True)
+            fl = FLAGS_DEFAULT if EXTRA else FLAGS
+            cmds.append([NVCC, *ARCH, *fl, f"-DNID_N={n}", "-c", os.path.join(CSRC, "kernels_aux.cu"), "-o", o])
     o = os.path.join(OBJ, "capi.o")
     objs.append(o)
     if force or _stale(o):

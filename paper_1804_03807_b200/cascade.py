@@ -34,13 +34,16 @@ from .tracker import (
     track_batch,
 )
 
+from . import refbridge
+
 GPU_MODES = ("gpu",)
 
 
-def _check_mode(mode: str):
-    if mode not in GPU_MODES:
-        raise ValueError(f"mode {mode!r}: this framework implements the GPU path only (mode='gpu'); "
-                         "the CPU work crew is the reference's")
+def _check_mode(mode: str) -> bool:
+    """True: track here on the GPU.  False: a CPU work-crew mode of the
+    reference ("thread" / "process"), which the caller delegates to nidpipe
+    (refbridge).  Anything else raises ValueError (parallel.py:109)."""
+    return refbridge.check_mode(mode)
 
 
 @dataclass
@@ -118,7 +121,8 @@ def solve_top(emb: EmbeddedSystem, p: int = 1, seed: int | None = None, params: 
     start instead (solve_start_system, cascade.py:110-160): the random-
     coefficient system g on the same supports, all cells tracked to g in one
     launch (`polyhedral.track_cells`), then g -> system from g's roots."""
-    _check_mode(mode)
+    if not _check_mode(mode):
+        return refbridge.solve_top(emb, p, seed, params, mode, cell_log)
     if cells is not None:
         return _solve_top_polyhedral(emb, seed, params, cells, cell_log, return_arrays, p)
     h, degrees = top_homotopy(emb, seed)
@@ -234,7 +238,8 @@ def _slack_removal_homotopy(emb: EmbeddedSystem, gamma: complex) -> LinearHomoto
 
 def cascade_step(level: CascadeLevel, p: int = 1, params: TrackParams = TrackParams(), mode: str = "gpu") -> CascadeLevel:
     """Track the level's nonzero-slack solutions one dimension down (cascade.py:296-322)."""
-    _check_mode(mode)
+    if not _check_mode(mode):
+        return refbridge.cascade_step(level, p, params, mode)
     if level.dimension < 1:
         raise ValueError("cannot cascade below dimension 0")
     emb = level.embedding
@@ -253,7 +258,8 @@ def cascade_step(level: CascadeLevel, p: int = 1, params: TrackParams = TrackPar
 def run_cascade(top_results, emb: EmbeddedSystem, p: int = 1, params: TrackParams = TrackParams(),
                 mode: str = "gpu") -> WitnessSuperset:
     """cascade.py:325-337"""
-    _check_mode(mode)
+    if not _check_mode(mode):
+        return refbridge.run_cascade(top_results, emb, p, params, mode)
     levels = [_classify_level(top_results, emb, emb.k, params)]
     while levels[-1].dimension > 0:
         levels.append(cascade_step(levels[-1], p, params, mode))

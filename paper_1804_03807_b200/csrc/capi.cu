@@ -81,6 +81,7 @@ struct NidHomotopy {
     h.rec = rec;
     h.runs = runs;
     for (int v = 0; v <= 16; ++v) h.grun[v] = grun[v];
+    h.dd = 0;
     return h;
   }
 };
@@ -120,6 +121,7 @@ typedef int (*RegsFn)();
 static const TrackFn k_track[17] = NID_TABLE(launch_track_);
 typedef int (*TrackPTFn)(const TrackArgsPT&, int, cudaStream_t);
 static const TrackPTFn k_track_pt[17] = NID_TABLE(launch_track_pt_);
+static const TrackFn k_track_aux[17] = NID_TABLE(launch_track_aux_);
 static const RegsFn k_pt_regs[17] = NID_TABLE(track_pt_regs_);
 static const EndpointFn k_endpoint[17] = NID_TABLE(launch_endpoint_);
 static const RefineFn k_refine[17] = NID_TABLE(launch_refine_);
@@ -533,12 +535,13 @@ int nid_last_counters(NidCounters* c) {
 // slot map for the workspace cache
 enum {
   W_STARTS = 0, W_PARAMS, W_XEND, W_STATUS, W_STEPS, W_TREACH, W_RESID, W_COND, W_REG,
-  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS, W_GSTATE, W_PTW
+  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS, W_GSTATE, W_PTW, W_TRACE, W_TRACEN
 };
 
 static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, long long first_index,
                       long long index_stride, const int32_t* degrees, const double* params, int param_div,
-                      const double* path_texp, NidPathOut* out, int device_io, void* stream);
+                      const double* path_texp, NidPathOut* out, int device_io, void* stream, int trace_cap = 0,
+                      double* trace = nullptr, int32_t* trace_n = nullptr);
 
 int nid_track_batch(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts,
                     long long first_index, const int32_t* degrees, const double* params, int param_div,
@@ -555,6 +558,14 @@ int nid_track_batch_strided(NidHomotopy* h, const NidTrackParams* prm, int P, co
                     stream);
 }
 
+int nid_track_trace(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, const double* params,
+                    int param_div, NidPathOut* out, int trace_cap, double* trace, int32_t* trace_n) {
+  if (!starts) FAIL("nid_track_trace needs explicit start points");
+  if (trace_cap < 1) FAIL("trace_cap must be >= 1");
+  return track_impl(h, prm, P, starts, 0, 1, nullptr, params, param_div, nullptr, out, 0, nullptr, trace_cap, trace,
+                    trace_n);
+}
+
 int nid_track_cells(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, const double* path_texp,
                     NidPathOut* out, int device_io, void* stream) {
   if (!h || !h->tw) FAIL("nid_track_cells needs a polyhedral homotopy (start_kind 2)");
@@ -564,8 +575,15 @@ int nid_track_cells(NidHomotopy* h, const NidTrackParams* prm, int P, const doub
 
 static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, long long first_index,
                       long long index_stride, const int32_t* degrees, const double* params, int param_div,
-                      const double* path_texp, NidPathOut* out, int device_io, void* stream) {
+                      const double* path_texp, NidPathOut* out, int device_io, void* stream, int trace_cap,
+                      double* trace, int32_t* trace_n) {
   if (!h || !prm || !out) FAIL("null argument");
+  if (prm->precision != 0 && prm->precision != 1) FAIL("precision must be 0 (double) or 1 (double_double)");
+  const bool use_aux = prm->precision == 1 || trace_cap > 0;
+  if (use_aux && (h->tw || path_texp))
+    FAIL("double-double tracking and step traces are not available for per-cell polyhedral homotopies");
+  if (trace_cap > 0 && (!trace || !trace_n)) FAIL("trace buffers missing");
+  if (trace_cap > 0 && device_io) FAIL("step traces are returned to host buffers only");
   BIND();
   if (index_stride < 1) FAIL("index_stride must be >= 1");
   if (P < 0) FAIL("negative path count");
@@ -574,6 +592,8 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   memset(&g_counters, 0, sizeof(g_counters));
   if (P == 0) return 0;
   if (!starts && !degrees) FAIL("need explicit starts or total-degree degrees");
+  if (trace_cap > 0 && (size_t)P * trace_cap * 3 * sizeof(double) > ((size_t)1 << 31))
+    FAIL("step trace: P * trace_cap too large (trace small batches)");
   if (h->tw && h->rec) FAIL("polyhedral homotopy: the streamed-record tracker does not evaluate t-weighted coefficients");
   if (h->tw && !starts) FAIL("polyhedral homotopy: explicit (binomial) start points are required");
   if (h->nparam > 0 && !params) FAIL("homotopy has per-path parameters but none were given");
@@ -685,13 +705,28 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   if (getenv("NID_LAT_STEPS")) a.lat_steps = atoi(getenv("NID_LAT_STEPS"));
   if (!a.gstate) FAIL("out of device memory (slot state)");
 
+  double* d_trace = nullptr;
+  int* d_trace_n = nullptr;
+  if (trace_cap > 0) {
+    d_trace = ws<double>(W_TRACE, (size_t)P * trace_cap * 3);
+    d_trace_n = ws<int>(W_TRACEN, P);
+    if (!d_trace || !d_trace_n) FAIL("out of device memory (step trace)");
+    CK(cudaMemsetAsync(d_trace_n, 0, (size_t)P * sizeof(int), s));
+    a.trace = d_trace;
+    a.trace_n = d_trace_n;
+    a.trace_cap = trace_cap;
+  }
+  a.H.dd = prm->precision == 1;
+
   Events ev;
   CK(cudaEventCreate(&ev.e[0]));
   CK(cudaEventCreate(&ev.e[1]));
   CK(cudaEventCreate(&ev.e[2]));
   cudaEvent_t e0 = ev.e[0], e1 = ev.e[1], e2 = ev.e[2];
   CK(cudaEventRecord(e0, s));
-  if (h->ptab && !getenv("NID_NO_PTAB")) {
+  if (use_aux) {
+    k_track_aux[n](a, max_blocks, s);
+  } else if (h->ptab && !getenv("NID_NO_PTAB")) {
     TrackArgsPT* pa = new TrackArgsPT;  // ~22 KB: off the stack
     pa->a = a;
     pa->t = *h->ptab;
@@ -708,6 +743,8 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   E.H = h->dev();
   E.P = P;
   E.dd_steps = prm->dd_refine_singular > 0 ? (prm->dd_refine_singular > 14 ? prm->dd_refine_singular : 14) : 0;
+  E.dd_mode = prm->precision == 1;
+  if (E.dd_mode) E.dd_steps = prm->dd_refine_singular > 3 ? prm->dd_refine_singular : 3;  // tracker.py:489
   E.params = d_params;
   E.param_div = param_div;
   E.x_end = d_x;
@@ -732,6 +769,10 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
     CK(cudaMemcpyAsync(out->residual, d_res, P * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(out->condition, d_cond, P * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(out->regular, d_reg, P, cudaMemcpyDeviceToHost, s));
+  }
+  if (trace_cap > 0) {
+    CK(cudaMemcpyAsync(trace, d_trace, (size_t)P * trace_cap * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(trace_n, d_trace_n, (size_t)P * sizeof(int), cudaMemcpyDeviceToHost, s));
   }
   unsigned long long hc[16];
   CK(cudaMemcpyAsync(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));

@@ -205,6 +205,11 @@ struct EndpointArgs {
   HomDev H;
   long long P;
   int dd_steps;  // 0 disables the polish
+  // double-double tracking (_track_dd, tracker.py:486-497): no cond > 1e4 polish
+  // inside _finish (the _DDView has no eval_generic); instead every endpoint is
+  // polished with dd_steps steps and taken when its double residual is finite
+  // and <= 4 x the endpoint residual
+  int dd_mode;
   const cd* params;
   int param_div;
   cd* x_end;
@@ -245,12 +250,12 @@ __global__ void __launch_bounds__(128) endpoint_kernel(EndpointArgs E) {
     int rank;
     eval_row<N>(E.H, g.lg, x, 1.0, prm, hv, J, sS, sT, false);
     group_cond_rank<N>(g, J, csl, cond, rank);
-    if (st == NID_CONVERGED && cond > 1e4 && E.dd_steps > 0) {
+    if (E.dd_mode ? E.dd_steps > 0 : (st == NID_CONVERGED && cond > 1e4 && E.dd_steps > 0)) {
       cd better[N];
       if (dd_polish<N>(g, E.H, prm, x, E.dd_steps, dsl, better)) {
         cd hb = eval_row_value<N>(E.H, g.lg, better, 1.0, prm);
         double res2 = group_nanmax<N>(g, cabsd(hb));
-        if (isfinite(res2) && res2 <= fmax(res * 4.0, 1e-14)) {
+        if (isfinite(res2) && res2 <= (E.dd_mode ? res * 4.0 : fmax(res * 4.0, 1e-14))) {
 #pragma unroll
           for (int v = 0; v < N; ++v) x[v] = better[v];
           res = res2;

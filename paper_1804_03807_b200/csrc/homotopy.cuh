@@ -62,6 +62,7 @@ struct HomDev {
   const TermRec* rec;
   const uint4* runs;
   int grun[17];
+  int dd;  // evaluate in complex double-double (auxiliary kernel, track_aux.cuh); set per launch
 };
 
 NID_D cd ldg_c(const cd* p) {

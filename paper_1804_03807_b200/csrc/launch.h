@@ -14,6 +14,7 @@ namespace nid {
 #define NID_DECL(n)                                                        \
   int launch_track_##n(const TrackArgs&, int, cudaStream_t);               \
   int launch_track_pt_##n(const TrackArgsPT&, int, cudaStream_t);          \
+  int launch_track_aux_##n(const TrackArgs&, int, cudaStream_t);           \
   int track_pt_regs_##n();                                                  \
   int launch_endpoint_##n(const EndpointArgs&, int, cudaStream_t);         \
   int launch_refine_##n(const RefineArgs&, int, cudaStream_t);             \

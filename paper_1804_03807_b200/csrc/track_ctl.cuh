@@ -309,7 +309,7 @@ __device__ NID_CLAIM_ATTR void load_start(const TrackArgs& Ar, long long path, c
 #else
 #define NID_CTL_ATTR __forceinline__
 #endif
-template <int N>
+template <int N, bool TR = false>
 __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, const cd* dxv) {
   constexpr int S = SLOTS;
   constexpr int DXST = (N + 1) * SLOTS;
@@ -471,6 +471,19 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
           DS_(D_PREV) = DS_(D_HSTEP);
           SETF(F_HAVEPREV, true);
           DS_(D_T) = DS_(D_TTRY);
+          if constexpr (TR) {  // trace.append((t, hstep, iters)) (tracker.py:393-394)
+            if (Ar.trace) {
+              const long long path = lsl[0];
+              const int k = Ar.trace_n[path];
+              if (k < Ar.trace_cap) {
+                double* rec = Ar.trace + ((size_t)path * Ar.trace_cap + k) * 3;
+                rec[0] = DS_(D_TTRY);
+                rec[1] = DS_(D_HSTEP);
+                rec[2] = (double)IS_(I_CITS);
+              }
+              Ar.trace_n[path] = k + 1;
+            }
+          }
           if (DS_(D_T) >= 1.0) {
             act = A_FINISH;
             continue;
@@ -681,7 +694,7 @@ struct has_table_flag<E, decltype((void)E::kTable)> {
 // table in global memory, read through L1) and the parameter-table kernel
 // (track_pt_kernel: csrc/track_ptab.cuh, the table in the launch's constant
 // bank).  Tab = void selects Eval; Tab = PTab selects PTEval.
-template <int N, class Eval, class Tab, bool PO = false>
+template <int N, class Eval, class Tab, bool PO = false, bool TR = false>
 __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) {
   using namespace ctl;
   using L = Lay<N>;
@@ -720,7 +733,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
 
   while (true) {
     NID_T0();
-    if (is_ctl) control<N>(Ar, V, augc + N * S);
+    if (is_ctl) control<N, TR>(Ar, V, augc + N * S);
     __syncwarp();
     {
       // |x_v| of the evaluation points of this warp's slots that need the

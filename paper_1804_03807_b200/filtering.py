@@ -20,6 +20,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
+from . import parallel, refbridge
 from .cascade import WitnessSuperset, _check_mode
 from .homotopy import LinearHomotopy, TrackParams, lower
 from .homotopy import DeviceHomotopy
@@ -120,7 +121,16 @@ def membership_batch(w: WitnessSet, Q, p: int = 1, params: TrackParams = TrackPa
 
     Returns (verdict int8 [C]: 1 member, 0 not, -1 indeterminate;
     paths_tracked)."""
-    _check_mode(mode)
+    if not _check_mode(mode):  # the reference decides candidate by candidate
+        v = np.zeros(len(Q), np.int8)
+        for i, q in enumerate(np.asarray(Q, dtype=np.complex128)):
+            try:
+                v[i] = 1 if refbridge.membership_test(w, q, p, params, mode) else 0
+            except Exception as e:  # the reference's MembershipIndeterminate
+                if type(e).__name__ != "MembershipIndeterminate":
+                    raise
+                v[i] = -1
+        return v, len(Q) * len(w.points)
     Q = np.asarray(Q, dtype=np.complex128)
     n = w.embedding.n_original
     if Q.ndim != 2 or Q.shape[1] != n:
@@ -155,6 +165,8 @@ def membership_batch(w: WitnessSet, Q, p: int = 1, params: TrackParams = TrackPa
 
 def membership_test(w: WitnessSet, q, p: int = 1, params: TrackParams = TrackParams(), mode: str = "gpu") -> bool:
     """filtering.py:92-127"""
+    if not _check_mode(mode):
+        return refbridge.membership_test(w, q, p, params, mode)
     q = np.asarray(q, dtype=np.complex128)
     n = w.embedding.n_original
     if q.shape != (n,):
@@ -218,7 +230,8 @@ def dedup(points: list, n: int | None = None) -> tuple[list, list]:
         return [], []
     order = sorted(range(len(points)), key=lambda i: points[i].residual)
     X = np.array([points[i].coordinates if n is None else points[i].coordinates[:n] for i in order])
-    pairs = match_pairs(X)
+    # a global view: decided on rank 0's GPU and broadcast
+    pairs = parallel.on_root(match_pairs, X)
     by_j: dict[int, list] = {}
     for i, j in pairs:
         by_j.setdefault(int(j), []).append(int(i))
@@ -241,7 +254,8 @@ def _dedup(points: list, n: int | None = None) -> list:
 
 def filter_junk(superset: WitnessSuperset, p: int = 1, params: TrackParams = TrackParams(), mode: str = "gpu"):
     """Top-down junk removal (filtering.py:153-201)."""
-    _check_mode(mode)
+    if not _check_mode(mode):
+        return refbridge.filter_junk(superset, p, params, mode)
     witness_sets: list[WitnessSet] = []
     stages: list[FilterStage] = []
     n = superset.embedding.n_original
@@ -272,7 +286,8 @@ def classify_isolated(candidates: list, witness_sets: list, base_system, p: int 
                       params: TrackParams = TrackParams(), mode: str = "gpu"):
     """Regular vs singular dimension-0 points, then the membership chain
     for the singular ones (filtering.py:204-256)."""
-    _check_mode(mode)
+    if not _check_mode(mode):
+        return refbridge.classify_isolated(candidates, witness_sets, base_system, p, params, mode)
     stages: list[FilterStage] = []
     regular: list[Solution] = []
     singular: list[Solution] = []

@@ -47,13 +47,12 @@ class TrackParams:
             raise ValueError(f"unknown precision {self.precision!r}")
 
     def to_c(self) -> _lib.TrackParamsC:
-        if self.precision != "double":
-            raise NotImplementedError("double-double tracking is not on the GPU path yet (SURVEY §8(f))")
         return _lib.TrackParamsC(
             self.initial_step, self.min_step, self.max_step, self.corrector_tol,
             int(self.max_corrector_iters), int(self.max_steps), self.infinity_threshold,
             self.endgame_start, self.endgame_contraction, self.snap_remaining,
-            int(self.final_newton_iters), int(self.dd_refine_singular), self.soft_infinity, 0, 0)
+            int(self.final_newton_iters), int(self.dd_refine_singular), self.soft_infinity,
+            1 if self.precision == "double_double" else 0, 0)
 
 
 def params_c(params) -> _lib.TrackParamsC:

@@ -139,5 +139,82 @@ def gather_finite(ctx: DistContext, x_end, status):
     return torch.cat([b[:c] for b, c in zip(blocks, counts)], dim=0)
 
 
+# ---------------------------------------------------------------- stage drivers
+#
+# The stage drivers (solve_top, cascade_step / run_cascade, membership_batch,
+# refine_batch) shard through one active context: every rank runs the same
+# host logic on the same inputs, tracks only its strided share of the stage's
+# paths (the reference's fan-outs cascade.py:229-230, :311-312,
+# filtering.py:114-115 split across processes), and one all_gather per stage
+# hands every rank the whole stage's records in job order -- which is also the
+# re-sharding for the next cascade level.  Classification that
+# needs a global view (dedup / multiplicity, filtering.py:140-150) runs on
+# rank 0 and its decision is broadcast (`on_root`).
+
+_ACTIVE: DistContext | None = None
+
+
+def activate(ctx: DistContext | None) -> None:
+    """Make ctx the context the stage drivers shard through (None: single rank)."""
+    global _ACTIVE
+    _ACTIVE = ctx
+
+
+def active() -> DistContext | None:
+    return _ACTIVE if _ACTIVE is not None and _ACTIVE.world > 1 else None
+
+
+def group_shard(ngroups: int, rank: int, world: int) -> np.ndarray:
+    """Strided share of `ngroups` job groups: r, r + world, ..."""
+    return np.arange(rank, int(ngroups), world, dtype=np.int64)
+
+
+def allgather_rows(ctx: DistContext, local: np.ndarray, ngroups: int) -> np.ndarray:
+    """Every rank holds the float64 rows of its strided share of `ngroups`
+    groups (local: [own groups, F]); returns all rows [ngroups, F] in group
+    order on every rank.  One padded all_gather (NCCL has no variable-count
+    gather); rows travel as raw bits, so NaN payloads survive."""
+    import torch
+    import torch.distributed as dist
+
+    local = np.ascontiguousarray(local, dtype=np.float64)
+    F = local.shape[1]
+    per = (int(ngroups) + ctx.world - 1) // ctx.world  # the largest share
+    dev = ctx._device()
+    pad = torch.zeros((per, F), dtype=torch.float64, device=dev)
+    if local.shape[0]:
+        pad[: local.shape[0]] = torch.from_numpy(local).to(dev)
+    blocks = [torch.empty_like(pad) for _ in range(ctx.world)]
+    dist.all_gather(blocks, pad)
+    out = np.empty((int(ngroups), F), np.float64)
+    for r, b in enumerate(blocks):
+        cnt = len(group_shard(ngroups, r, ctx.world))
+        out[r::ctx.world] = b[:cnt].cpu().numpy()
+    return out
+
+
+def allreduce_sum(ctx: DistContext, values) -> list:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=ctx._device())
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [int(v) for v in t.tolist()]
+
+
+def on_root(fn, *args):
+    """Run fn(*args) on rank 0 only and broadcast its (picklable) result, so a
+    decision taken from a global view is the same on every rank.  Without an
+    active multi-rank context this is just fn(*args)."""
+    ctx = active()
+    if ctx is None:
+        return fn(*args)
+    import torch.distributed as dist
+
+    box = [fn(*args) if ctx.rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
 def merge_shards(parts: list[np.ndarray]) -> np.ndarray:
     return np.concatenate(parts, axis=0) if parts else np.zeros((0,))

@@ -224,7 +224,22 @@ def solve_cell(cell, g, supports, params: TrackParams = TrackParams(), mode: str
 
     starts = cell_starts(cell, g)
     h = PolyhedralHomotopy(g, cell, tuple(supports))
-    return track_batch(h, starts, params).path_results()
+    return track_batch(h, starts, _cell_params(params)).path_results()
+
+
+def _cell_params(params):
+    """Cells are tracked in double precision whatever params.precision says:
+    the reference's PolyhedralHomotopy evaluates generically (double-double)
+    only at t = 1 (polyhedral.py:783-791), so its double-double mode cannot
+    track a cell; the start roots are polished by the continuation that
+    follows."""
+    if getattr(params, "precision", "double") == "double":
+        return params
+    from dataclasses import fields as _fields
+
+    kw = {f.name: getattr(params, f.name) for f in _fields(TrackParams) if hasattr(params, f.name)}
+    kw["precision"] = "double"
+    return TrackParams(**kw)
 
 
 def track_cells(cells, g, supports, params: TrackParams = TrackParams()):
@@ -260,7 +275,7 @@ def track_cells(cells, g, supports, params: TrackParams = TrackParams()):
     o = _lib.PathOutC(_lib.ptr(out.x), _lib.ptr(out.status), _lib.ptr(out.steps), _lib.ptr(out.t_reached),
                       _lib.ptr(out.residual), _lib.ptr(out.condition), _lib.ptr(out.regular))
     L = _lib.lib()
-    pc = params_c(params)
+    pc = params_c(_cell_params(params))
     _lib.check(L.nid_track_cells(dev.handle, C.byref(pc), P, _lib.ptr(st), _lib.ptr(tw), C.byref(o), 0, None), L)
     out.counters = _lib.last_counters()
     return out, counts

@@ -80,6 +80,7 @@ class TrackResults:
     condition: np.ndarray
     regular: np.ndarray  # 1 regular, 0 singular, -1 none
     counters: dict
+    traces: list | None = None  # per path [(t, step, corrector iterations), ...] when requested
 
     def __len__(self):
         return int(self.status.size)
@@ -126,16 +127,94 @@ def _device_of(h) -> DeviceHomotopy:
 _FOREIGN: dict = {}
 
 
+_TRACK_FIELDS = ("t_reached", "residual", "condition", "status", "steps", "regular")
+_SUM_COUNTERS = ("evals", "jacs", "scales", "paths", "dd_polished", "lstsq_fallbacks")
+
+
 def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=None, first_index: int = 0,
                 count: int | None = None, index_stride: int = 1, target_params=None, param_div: int = 1,
-                out: TrackResults | None = None) -> TrackResults:
+                out: TrackResults | None = None, trace: bool = False) -> TrackResults:
+    """`_track_local` on one rank.  Under an active multi-rank context
+    (`parallel.activate`) every rank tracks its strided share of the job
+    groups (a group = param_div consecutive paths, e.g. one membership
+    candidate's paths) and one all_gather returns the whole batch's records,
+    in job order, on every rank: the GPU form of the reference's fan-outs
+    cascade.py:229-230, :311-312 and filtering.py:114-115 across processes."""
+    from . import parallel
+
+    ctx = parallel.active()
+    if ctx is None or out is not None or trace:
+        return _track_local(h, starts, params, degrees=degrees, first_index=first_index, count=count,
+                            index_stride=index_stride, target_params=target_params, param_div=param_div, out=out,
+                            trace=trace)
+    n = _dim_of(h)
+    d = max(1, int(param_div))
+    if starts is not None:
+        st = np.ascontiguousarray(starts, dtype=np.complex128).reshape(-1, n)
+        P = st.shape[0]
+    else:
+        if degrees is None or count is None:
+            raise ValueError("give start points, or degrees and count for total-degree starts")
+        if d != 1:
+            raise ValueError("device-generated starts shard path by path (param_div must be 1)")
+        st, P = None, int(count)
+    if P % d:
+        raise ValueError("path count must be a multiple of param_div")
+    G = P // d
+    mine = parallel.group_shard(G, ctx.rank, ctx.world)
+    kw = dict(param_div=d)
+    if st is not None:
+        kw["starts"] = st.reshape(G, d, n)[mine].reshape(-1, n)
+    else:
+        kw.update(starts=None, degrees=degrees, count=len(mine), first_index=first_index + ctx.rank * index_stride,
+                  index_stride=index_stride * ctx.world)
+    if target_params is not None:
+        tp = np.ascontiguousarray(target_params, dtype=np.complex128)
+        kw["target_params"] = tp.reshape(G, -1)[mine]
+    if len(mine):
+        loc = _track_local(h, kw.pop("starts"), params, **kw)
+    else:
+        loc = TrackResults(np.empty((0, n), np.complex128), np.empty(0, np.int8), np.empty(0, np.int32), np.empty(0),
+                           np.empty(0), np.empty(0), np.empty(0, np.int8), dict.fromkeys(_SUM_COUNTERS, 0))
+    # one row per group: [x (2 n d) | the six scalar fields (d each)]
+    rows = np.concatenate([loc.x.view(np.float64).reshape(len(mine), -1)] +
+                          [np.asarray(getattr(loc, f), np.float64).reshape(len(mine), d) for f in _TRACK_FIELDS], axis=1)
+    full = parallel.allgather_rows(ctx, rows, G)
+    x = np.ascontiguousarray(full[:, : 2 * n * d]).view(np.complex128).reshape(P, n)
+    cols = [full[:, 2 * n * d + i * d: 2 * n * d + (i + 1) * d].reshape(P) for i in range(len(_TRACK_FIELDS))]
+    res = TrackResults(x, cols[3].astype(np.int8), cols[4].astype(np.int32), cols[0].copy(), cols[1].copy(),
+                       cols[2].copy(), cols[5].astype(np.int8), {})
+    sums = parallel.allreduce_sum(ctx, [loc.counters.get(k, 0) for k in _SUM_COUNTERS])
+    res.counters = dict(zip(_SUM_COUNTERS, sums))
+    res.counters["kernel_ms_track"] = ctx.max_over_ranks(loc.counters.get("kernel_ms_track", 0.0))
+    res.counters["kernel_ms_endpoint"] = ctx.max_over_ranks(loc.counters.get("kernel_ms_endpoint", 0.0))
+    res.counters["ranks"] = ctx.world
+    return res
+
+
+def _dim_of(h) -> int:
+    if hasattr(h, "n"):
+        return int(h.n)
+    if hasattr(h, "dim"):
+        return int(h.dim)
+    return int(h.target.nvars)
+
+
+def _track_local(h, starts=None, params: TrackParams = TrackParams(), *, degrees=None, first_index: int = 0,
+                 count: int | None = None, index_stride: int = 1, target_params=None, param_div: int = 1,
+                 out: TrackResults | None = None, trace: bool = False) -> TrackResults:
     """Track many paths of h in one launch.
 
     starts: [P, n] start points, or None with `degrees` for total-degree
     starts generated on the device for path indices first_index + i * index_stride,
     i < count.
     target_params: per-path target coefficients ([P/param_div, nparam]) for
-    homotopies lowered with parameter slots (membership tests)."""
+    homotopies lowered with parameter slots (membership tests).
+    trace: also record every path's accepted steps (explicit starts only;
+    small batches); `out.traces[i]` is then the list of (t, step, corrector
+    iterations) tuples the reference's trace hook receives (tracker.py:393-394).
+    params.precision == "double_double" tracks with every evaluation in
+    complex double-double (tracker.py:458-497)."""
     L = _lib.lib()
     dev = _device_of(h)
     n = dev.n
@@ -157,18 +236,31 @@ def track_batch(h, starts=None, params: TrackParams = TrackParams(), *, degrees=
     o = _lib.PathOutC(_lib.ptr(out.x), _lib.ptr(out.status), _lib.ptr(out.steps), _lib.ptr(out.t_reached),
                       _lib.ptr(out.residual), _lib.ptr(out.condition), _lib.ptr(out.regular))
     pc = params_c(params)
-    _lib.check(L.nid_track_batch_strided(dev.handle, C.byref(pc), P, _lib.ptr(st), int(first_index),
-                                         int(index_stride), _lib.ptr(deg), _lib.ptr(prm), int(param_div),
-                                         C.byref(o), 0, None), L)
+    if trace:
+        if st is None:
+            raise ValueError("step traces need explicit start points")
+        cap = max(1, int(pc.max_steps))
+        tr = np.zeros((P, cap, 3), np.float64)
+        tn = np.zeros(P, np.int32)
+        _lib.check(L.nid_track_trace(dev.handle, C.byref(pc), P, _lib.ptr(st), _lib.ptr(prm), int(param_div),
+                                     C.byref(o), cap, _lib.ptr(tr), _lib.ptr(tn)), L)
+        out.traces = [[(float(t), float(hs), int(it)) for t, hs, it in tr[i, :min(int(tn[i]), cap)]]
+                      for i in range(P)]
+    else:
+        _lib.check(L.nid_track_batch_strided(dev.handle, C.byref(pc), P, _lib.ptr(st), int(first_index),
+                                             int(index_stride), _lib.ptr(deg), _lib.ptr(prm), int(param_div),
+                                             C.byref(o), 0, None), L)
     out.counters = _lib.last_counters()
     return out
 
 
 def track(h, x0, params: TrackParams = TrackParams(), trace: list | None = None) -> PathResult:
-    """Track one path (tracker.py:341-407) -- a batch of one on the GPU."""
+    """Track one path (tracker.py:341-407) -- a batch of one on the GPU.  A
+    trace list receives (t, step, corrector_iterations) per accepted step."""
+    res = track_batch(h, np.asarray(x0, dtype=np.complex128)[None], params, trace=trace is not None)
     if trace is not None:
-        raise NotImplementedError("per-step traces are not recorded by the GPU tracker")
-    return track_batch(h, np.asarray(x0, dtype=np.complex128)[None], params).result(0)
+        trace.extend(res.traces[0])
+    return res.result(0)
 
 
 def newton_step(J, r):
@@ -235,6 +327,29 @@ class RefineResults:
 
 def refine_batch(f: PolySystem, X, tol: float = 1e-12, max_iters: int = 10, n_original: int | None = None,
                  infinity_threshold: float = 1e8, h: LinearHomotopy | None = None) -> RefineResults:
+    """`_refine_local`; under an active multi-rank context the points are
+    sharded like the paths of track_batch and gathered back in order."""
+    from . import parallel
+
+    ctx = parallel.active()
+    if ctx is None:
+        return _refine_local(f, X, tol, max_iters, n_original, infinity_threshold, h)
+    n = f.nvars
+    X = np.array(X, dtype=np.complex128).reshape(-1, n)
+    P = X.shape[0]
+    mine = parallel.group_shard(P, ctx.rank, ctx.world)
+    loc = _refine_local(f, X[mine], tol, max_iters, n_original, infinity_threshold, h)
+    rows = np.concatenate([loc.x.view(np.float64).reshape(len(mine), 2 * n)] +
+                          [np.asarray(a, np.float64).reshape(len(mine), 1)
+                           for a in (loc.residual, loc.condition, loc.regular, loc.rank, loc.slack)], axis=1)
+    full = parallel.allgather_rows(ctx, rows, P)
+    c = full[:, 2 * n:]
+    return RefineResults(np.ascontiguousarray(full[:, : 2 * n]).view(np.complex128).reshape(P, n), c[:, 0].copy(),
+                         c[:, 1].copy(), c[:, 2].astype(np.int8), c[:, 3].astype(np.int32), c[:, 4].astype(np.int8))
+
+
+def _refine_local(f: PolySystem, X, tol: float = 1e-12, max_iters: int = 10, n_original: int | None = None,
+                  infinity_threshold: float = 1e8, h: LinearHomotopy | None = None) -> RefineResults:
     """newton_refine + classify for many points in one launch."""
     h = h or system_homotopy(f)
     dev = h.device()
@@ -259,6 +374,22 @@ def newton_refine(f: PolySystem, x, tol: float = 1e-12, max_iters: int = 10) -> 
 
 
 def refine_dd_batch(f: PolySystem, X, steps: int = 3, h: LinearHomotopy | None = None):
+    """refine_dd for many points; sharded under an active multi-rank context."""
+    from . import parallel
+
+    ctx = parallel.active()
+    if ctx is None:
+        return _refine_dd_local(f, X, steps, h)
+    n = f.nvars
+    X = np.array(X, dtype=np.complex128).reshape(-1, n)
+    mine = parallel.group_shard(len(X), ctx.rank, ctx.world)
+    lx, lok = _refine_dd_local(f, X[mine], steps, h)
+    rows = np.concatenate([lx.view(np.float64).reshape(len(mine), 2 * n), lok.astype(np.float64).reshape(-1, 1)], axis=1)
+    full = parallel.allgather_rows(ctx, rows, len(X))
+    return (np.ascontiguousarray(full[:, : 2 * n]).view(np.complex128).reshape(len(X), n), full[:, 2 * n].astype(np.int8))
+
+
+def _refine_dd_local(f: PolySystem, X, steps: int = 3, h: LinearHomotopy | None = None):
     h = h or system_homotopy(f)
     dev = h.device()
     X = np.array(X, dtype=np.complex128).reshape(-1, dev.n)

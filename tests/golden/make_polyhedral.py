@@ -142,6 +142,13 @@ def decompose_golden(name, pd):
         out[f"c{ci}_texps"] = np.concatenate([np.asarray(t, float) for t in cell.texps])
         out[f"c{ci}_volume"] = np.int32(cell.volume)
     np.savez_compressed(os.path.join(HERE, f"decompose_{name}.npz"), **out)
+    # the reference's own deterministic JSON report of that run (report.py:81-128)
+    import nidpipe.report as rr
+
+    with open(os.path.join(HERE, f"report_{name}.json"), "w", encoding="utf-8") as fh:
+        fh.write(rr.report_to_json(rep))
+    with open(os.path.join(HERE, f"summary_{name}.txt"), "w", encoding="utf-8") as fh:
+        fh.write(rr.summary_text(rep).split("timings:")[0])
 
 
 if __name__ == "__main__" and os.environ.get("POLY_DECOMPOSE", "0") == "1":

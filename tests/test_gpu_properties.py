@@ -60,3 +60,49 @@ def test_multiplicity_of_double_point_matches_oracle(nid):
     rkept, rmult = O.dedup(rpts)
     assert sorted(mult) == sorted(rmult)
     assert len(pts) == len(rpts)
+
+
+@pytest.mark.parametrize("which", ["c2_parameter_bank", "c3mini_table", "c3_records_latency_mode"])
+def test_results_do_not_depend_on_slot_neighbours_or_schedule(nid, which):
+    """Race check by construction (compute-sanitizer is closed on this GPU
+    pool, profiles/compute_sanitizer_closed_r02.log): a path's record must not
+    depend on which block / slot / neighbours it ran with or on when its slot
+    was refilled.  The same start points tracked in their order, in a random
+    permutation and in a second random permutation interleaved with other
+    paths give bit-identical endpoints, statuses, step counts and residuals
+    path by path.  A missing barrier / __syncwarp or a slot-indexing bug in
+    the [item][slot] shared-memory layout shows up here as a difference."""
+    from paper_1804_03807_b200 import cascade, systems
+
+    rng = np.random.default_rng(12)
+    if which == "c2_parameter_bank":
+        p = configs.c2()
+        h = LinearHomotopy(p.start, p.target, p.gamma)
+        starts = systems.total_degree_starts(p.degrees, 0, 3000)
+    elif which == "c3mini_table":
+        pd = configs.c3_mini()
+        h, deg = cascade.top_homotopy(pd.emb)
+        starts = systems.total_degree_starts(deg)
+    else:  # n = 14 streamed records; the small launch puts paths past 64 steps in per-slot mode
+        pd = configs.c3()
+        h, deg = cascade.top_homotopy(pd.emb)
+        starts = systems.total_degree_starts_at(deg, np.sort(rng.choice(65536, 600, replace=False)))
+    base = tracker.track_batch(h, starts)
+    for trial in range(2):
+        perm = rng.permutation(len(starts))
+        if trial == 1:  # interleave with foreign paths: different neighbours and refill order
+            extra = starts[rng.integers(0, len(starts), len(starts) // 2)]
+            mixed = np.concatenate([starts[perm], extra])
+            order = rng.permutation(len(mixed))
+            res = tracker.track_batch(h, mixed[order])
+            inv = np.empty(len(mixed), np.int64)
+            inv[order] = np.arange(len(mixed))
+            pick = inv[: len(starts)]
+        else:
+            res = tracker.track_batch(h, starts[perm])
+            pick = np.arange(len(starts))
+        assert np.array_equal(res.status[pick], base.status[perm])
+        assert np.array_equal(res.steps[pick], base.steps[perm])
+        assert np.array_equal(res.x[pick], base.x[perm], equal_nan=True)
+        assert np.array_equal(res.residual[pick], base.residual[perm], equal_nan=True)
+        assert np.array_equal(res.t_reached[pick], base.t_reached[perm])

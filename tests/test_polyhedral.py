@@ -329,9 +329,9 @@ def test_decompose_argument_checks():
     with pytest.raises(ValueError):
         blackbox.decompose(f, top_dimension=f.nvars, cells=[])
     with pytest.raises(ValueError):
-        blackbox.decompose(f, top_dimension=2, precision="dd", cells=[])
+        blackbox.decompose(f, top_dimension=2, precision="quad", cells=[])
     with pytest.raises(ValueError):
-        blackbox.decompose(f, top_dimension=2, mode="thread", cells=[])
+        blackbox.decompose(f, top_dimension=2, mode="fpga", cells=[])
     nonsquare = PolySystem(f.nvars, f.polys[:-1])
     with pytest.raises(ValueError):
         blackbox.decompose(nonsquare, top_dimension=2, cells=[])
