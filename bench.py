@@ -140,16 +140,34 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(load)), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
 
 
+NOMINAL_FP64 = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2 TFLOP/s: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
+
+
 def fp64_peak():
+    """(peak, source): the measured DFMA-chain peak of this pool's B200s
+    (tools/fp64_peak.cu, profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has
+    no FP64 entry), else the nominal figure.  The JSON line states both."""
     p = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
     try:
         for line in open(p):
             d = json.loads(line)
             if "fp64_tflops_sustained" in d:
-                return float(d["fp64_tflops_sustained"]), "measured DFMA peak on this pool's B200 (tools/fp64_peak.cu)"
+                return float(d["fp64_tflops_sustained"]), ("measured DFMA peak on this pool's B200 at 1965 MHz "
+                                                           "(tools/fp64_peak.cu, profiles/fp64_peak_r01.json)")
     except Exception:
         pass
-    return 37.2, "nominal 148 SM x 64 FMA x 2 x 1.965 GHz (no measurement found)"
+    return NOMINAL_FP64, "nominal 148 SM x 64 FMA x 2 x 1.965 GHz (no measurement found)"
+
+
+def measured_traffic():
+    """DRAM bytes of the full 3,628,800-path launch of the tracker kernel from
+    the ncu capture of exactly that launch (profiles/track_traffic_r02.json);
+    scaled by the rank's share of the paths under sharding.  None if absent."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "track_traffic_r02.json")))
+        return float(d["dram_bytes_total"]), int(d["paths"])
+    except Exception:
+        return None, None
 
 
 def native_arm(args, prob):
@@ -261,13 +279,9 @@ def native_arm(args, prob):
                "sample": f"{args.cpu_sample} seeded uniform C5 path indices, oracle/nid_oracle.py "
                          f"(numpy restatement of nidpipe.tracker.track) on {cores} processes"}
 
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "track_traffic_r01ff.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic, tpaths = measured_traffic()
+    if traffic is not None:
+        traffic = traffic * Pl / tpaths  # this rank's launch (the capture is the whole C5 launch)
 
     if ctx.rank == 0:
         line = {
@@ -283,7 +297,10 @@ def native_arm(args, prob):
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "track_pt_kernel<10, false>",
-                         "peak_source": peak_src,
+                         "peak_source": peak_src, "peak_nominal": NOMINAL_FP64,
+                         "frac_of_nominal": achieved / NOMINAL_FP64,
+                         "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of the full C5 launch "
+                                           "(profiles/track_traffic_r02.json)",
                          "algorithmic_flop_per_launch": flop, "kernel_ms_per_launch": k_ms,
                          "endpoint_kernel_ms_per_launch": e_ms, "share_of_step": k_ms / (ms / args.steps),
                          "counts_per_path": {"eval": ev / Pl, "jac": jc / Pl, "scale": sc / Pl},
@@ -291,6 +308,100 @@ def native_arm(args, prob):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
+def stage_arm(args):
+    """--workload c3 / c4: the other two full-size configs through the public
+    stage drivers (host buffers in, records out: every number here is end to
+    end).  One step of c3 = solve_top (65,536 paths) + run_cascade (6 levels)
+    + filter_junk; of c4 = membership_batch of the candidates against the
+    degree-4 witness set (4 paths each).  Under torchrun the stage drivers
+    shard through parallel.activate (strided groups + one all_gather per
+    stage).  Reported: paths/s over every path tracked in the step, wall clock
+    around the synchronous driver calls, max over ranks."""
+    import torch
+
+    from paper_1804_03807_b200 import cascade, configs, filtering, flops, parallel
+    from paper_1804_03807_b200.homotopy import TrackParams
+
+    ctx = parallel.DistContext.from_env(args.gpus)
+    torch.cuda.set_device(ctx.local_rank)
+    parallel.activate(ctx)
+    pd = configs.c3()
+    params = TrackParams()
+    info = {}
+    if args.workload == "c4":
+        top, _ = cascade.solve_top(pd.emb, return_arrays=True)
+        lv = cascade._classify_level(top, pd.emb, pd.emb.k, params)
+        W = filtering.WitnessSet(pd.emb.k, pd.emb, lv.zero_slack)
+        half = args.c4_candidates // 2
+        cands, labels, _ = configs.c4_candidates(pd, half, args.c4_candidates - half, 44)
+        mh = filtering.MembershipHomotopy(W)
+
+    def step():
+        if args.workload == "c3":
+            t0 = time.perf_counter()
+            top, st = cascade.solve_top(pd.emb, return_arrays=True)
+            c = top.counters
+            t1 = time.perf_counter()
+            sup = cascade.run_cascade(top, pd.emb, 1, params)
+            t2 = time.perf_counter()
+            wsets, stages = filtering.filter_junk(sup, 1, params)
+            t3 = time.perf_counter()
+            paths = len(top) + sum(lv.starts for lv in sup.levels[1:]) + sum(s.paths_tracked for s in stages)
+            info.update(top_s=t1 - t0, cascade_s=t2 - t1, filter_s=t3 - t2, top_kernel_ms=c["kernel_ms_track"],
+                        top_counters=c, levels=[lv.counts for lv in sup.levels],
+                        degrees={w.dimension: w.degree for w in wsets})
+            return paths
+        verdict, tracked = filtering.membership_batch(W, cands, 1, params, mh=mh)
+        info.update(agree=float(np.mean((verdict == 1) == (labels == 1))), indeterminate=int(np.sum(verdict < 0)),
+                    on_component=int(np.sum(verdict == 1)))
+        return tracked
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    with ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_bench_r{ctx.rank}.csv")
+                      if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp/nid_clocks.csv") as clk:
+        t0 = time.perf_counter()
+        paths = 0
+        for _ in range(args.steps):
+            paths = step()
+        torch.cuda.synchronize()
+        dt = ctx.max_over_ranks(time.perf_counter() - t0)
+    value = paths * args.steps / dt
+    if ctx.rank == 0:
+        roof = None
+        if args.workload == "c3":
+            from paper_1804_03807_b200.cascade import top_homotopy
+
+            fm = flops.flop_model(top_homotopy(pd.emb)[0].lowered())
+            c = info.pop("top_counters")
+            fl = fm.total(c["evals"], c["jacs"], c["scales"])
+            peak, src = fp64_peak()
+            ach = fl / (info["top_kernel_ms"] / 1e3) / 1e12
+            roof = {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": None, "kernel": "track_ctl_kernel<14> (top continuation, 65,536 paths)",
+                    "peak_source": src, "peak_nominal": NOMINAL_FP64, "flop_model": fm.as_dict()}
+        names = {"c3": "C3 positive-dimensional n=8 (+6 slack): solve_top 65,536 paths + 6 cascade levels + "
+                       "filter_junk (BASELINE configs[2])",
+                 "c4": f"C4 membership: {args.c4_candidates} candidates x 4 witness paths (BASELINE configs[3])"}
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": names[args.workload], "paths_per_step": paths, "seed": 3,
+                       "track_params": "reference defaults (tracker.py:113-127)",
+                       "l2": "per-step inputs and records exceed L2 only for c4; c3 stages are latency bound",
+                       **{k: v for k, v in info.items()}},
+            "clocks": clk.summary(ctx.local_rank),
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                    "timing": "wall clock around the public stage drivers (host buffers), max over ranks"},
+            "roofline": roof, "cpu_baseline": None}), flush=True)
+    parallel.activate(None)
     ctx.close()
     return 0
 
@@ -306,9 +417,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=480)
     ap.add_argument("--ref-sample", type=int, default=160)
+    ap.add_argument("--workload", choices=["c5", "c3", "c4"], default="c5",
+                    help="c5 (default, the headline config), c3 (top + cascade + filter), c4 (membership)")
+    ap.add_argument("--c4-candidates", type=int, default=100000)
     args = ap.parse_args()
     from paper_1804_03807_b200 import configs
 
+    if args.workload != "c5":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the C5 workload only"}))
+            return 0
+        return stage_arm(args)
     prob = configs.c5()
     if args.impl == "reference":
         return reference_arm(args, prob)

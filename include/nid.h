@@ -27,6 +27,8 @@
  *   nid_refine_batch      newton_refine + classify                     tracker.py:410-455
  *   nid_dd_refine_batch   refine_dd                                    tracker.py:431-435
  *   nid_match_pairs       points_match over all pairs (for _dedup)     filtering.py:73-78,140-150
+ *   nid_init_devices / nid_use_device / nid_compact_finite / nid_gather_endpoints
+ *                         the work crew across GPUs: results re-united    parallel.py:91-106,131-134
  */
 #ifndef NID_H
 #define NID_H
@@ -127,6 +129,17 @@ int nid_device_count(int* count);
 int nid_init(int device);
 int nid_shutdown(void);
 
+/* Several GPUs in one process (the one-process-per-GPU
+ * launch uses nid_init and torch.distributed instead).  nid_init_devices
+ * creates a context on every listed CUDA device and enables peer access
+ * between them; nid_use_device(i) makes devs[i] the calling thread's current
+ * device for the handles it creates next.  A handle remembers its device and
+ * every call on it runs there, so a host thread per device can track its
+ * shard (nid_track_batch_strided with first_index = i, index_stride = ndev)
+ * concurrently. */
+int nid_init_devices(int ndev, const int* devs);
+int nid_use_device(int i);
+
 int nid_homotopy_create(const NidHomotopyDesc* desc, NidHomotopy** out);
 int nid_homotopy_destroy(NidHomotopy* h);
 
@@ -198,6 +211,23 @@ int nid_dd_refine_batch(NidHomotopy* h, int P, double* x, int steps, int8_t* ok)
  * *npairs gets the total count (may exceed capacity). */
 int nid_match_pairs(int n, int ncmp, int P, const double* X, int32_t* pairs, long long max_pairs,
                     long long* npairs);
+
+/* The endpoint exchange of a stage (the reference has no
+ * counterpart: its work crew returns results through one process's memory,
+ * parallel.py:91-106).  nid_compact_finite: on the current device, the
+ * succeeded (converged / singular_endpoint) endpoints of x_end[P*n*2] in path
+ * order into x_out, with their global path indices first_index + i *
+ * index_stride in index_out (or NULL); device pointers.
+ * nid_gather_endpoints: the same for nparts shards living on the devices
+ * part_device[p] (indices into nid_init_devices' list), each compacted on its
+ * own GPU and copied peer to peer (NVLink) into x_out / index_out on the root
+ * device, part after part; *total = endpoints gathered. */
+int nid_compact_finite(int n, long long P, const double* x_end, const int8_t* status, long long first_index,
+                       long long index_stride, double* x_out, long long* index_out, long long capacity,
+                       long long* count, void* stream);
+int nid_gather_endpoints(int nparts, const int* part_device, const double* const* x_end, const int8_t* const* status,
+                         const long long* counts, const long long* first_index, const long long* index_stride, int n,
+                         int root_device, double* x_out, long long* index_out, long long capacity, long long* total);
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,8 @@ EXPORTS = (
     "nid_last_error", "nid_device_count", "nid_init", "nid_shutdown", "nid_homotopy_create",
     "nid_homotopy_destroy", "nid_eval_batch", "nid_newton_step_batch", "nid_svd_batch",
     "nid_track_batch", "nid_track_batch_strided", "nid_last_counters", "nid_refine_batch", "nid_dd_refine_batch",
-    "nid_match_pairs", "nid_track_cells", "nid_track_trace",
+    "nid_match_pairs", "nid_track_cells", "nid_track_trace", "nid_init_devices", "nid_use_device",
+    "nid_compact_finite", "nid_gather_endpoints",
 )
 
 
@@ -95,6 +96,10 @@ def load_library():
             "nid_track_batch_strided": ([p, p, i, p, ll, ll, p, p, i, p, i, p], i),
             "nid_track_cells": ([p, p, i, p, p, p, i, p], i),
             "nid_track_trace": ([p, p, i, p, p, i, p, i, p, p], i),
+            "nid_init_devices": ([i, p], i),
+            "nid_use_device": ([i], i),
+            "nid_compact_finite": ([i, ll, p, p, ll, ll, p, p, ll, p, p], i),
+            "nid_gather_endpoints": ([i, p, p, p, p, p, p, i, i, p, p, ll, p], i),
             "nid_last_counters": ([p], i),
             "nid_refine_batch": ([p, i, p, d, i, i, d, p, p, p, p, p], i),
             "nid_dd_refine_batch": ([p, i, p, i, p], i),

@@ -59,3 +59,37 @@ __global__ void match_tol_kernel(int n, int ncmp, long long P, const cd* X, doub
   for (int v = 0; v < ncmp; ++v) s = nanmax(s, cabsd(X[i * n + v]));
   tolb[i] = fmax(1e-8, 1e-6 * s);
 }
+
+// K7 pre-pass: order-preserving compaction of the succeeded endpoints
+// (status converged / singular_endpoint) of one shard -- what a rank sends to
+// the classification rank.  256 paths per block: pass 1
+// counts per block, the host scans the block counts, pass 2 writes each
+// block's endpoints at its offset (ballot ranks inside the warp, warp totals
+// through shared memory), with the path's global index
+// first_index + i * index_stride.
+__global__ void __launch_bounds__(256) finite_count_kernel(long long P, const int8_t* status, int* block_counts) {
+  const long long i = (long long)blockIdx.x * 256 + threadIdx.x;
+  const int st = i < P ? status[i] : NID_FAILED;
+  const int cnt = __syncthreads_count(st == NID_CONVERGED || st == NID_SINGULAR_ENDPOINT);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = cnt;
+}
+
+__global__ void __launch_bounds__(256) finite_compact_kernel(long long P, int n, const cd* x, const int8_t* status,
+                                                             const long long* block_off, long long first_index,
+                                                             long long index_stride, cd* out, long long* index_out) {
+  __shared__ int wtot[8];
+  const long long i = (long long)blockIdx.x * 256 + threadIdx.x;
+  const int st = i < P ? status[i] : NID_FAILED;
+  const bool keep = st == NID_CONVERGED || st == NID_SINGULAR_ENDPOINT;
+  const unsigned m = __ballot_sync(0xffffffffu, keep);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) wtot[w] = __popc(m);
+  __syncthreads();
+  int base = 0;
+  for (int k = 0; k < w; ++k) base += wtot[k];
+  if (keep) {
+    const long long dst = block_off[blockIdx.x] + base + __popc(m & ((1u << lane) - 1u));
+    for (int v = 0; v < n; ++v) out[dst * n + v] = x[i * n + v];
+    if (index_out) index_out[dst] = first_index + i * index_stride;
+  }
+}

@@ -19,7 +19,11 @@
 static thread_local std::string g_err;
 static NidCounters g_counters = {};
 static unsigned long long g_phase[7] = {};
-static int g_device = -1;
+static int g_device = -1;          // the process default (nid_init)
+static thread_local int t_device = -1;  // this host thread's choice (nid_use_device / a handle's device)
+static int g_devs[16];
+static int g_ndev = 0;
+static int cur_device() { return t_device >= 0 ? t_device : g_device; }
 
 #define FAIL(msg)          \
   do {                     \
@@ -40,6 +44,7 @@ static_assert(sizeof(NidHomotopyDesc) == 96, "NidHomotopyDesc layout changed");
 static_assert(sizeof(NidTrackParams) == 96, "NidTrackParams layout changed");
 
 struct NidHomotopy {
+  int device = -1;  // the CUDA device the table lives on (every call on the handle runs there)
   int n, nterms, nparam, maxdeg, multilinear, td;
   int tddeg[NID_MAX_VARS];
   int grow[NID_MAX_VARS];
@@ -91,11 +96,12 @@ struct Buf {
   void* p = nullptr;
   size_t cap = 0;
 };
-static Buf g_bufs[32];
+static Buf g_bufs[16][32];  // per CUDA device
 template <class T>
 static T* ws(int slot, size_t count) {
   size_t bytes = count * sizeof(T) + 16;
-  Buf& b = g_bufs[slot];
+  const int d = cur_device();
+  Buf& b = g_bufs[(d >= 0 && d < 16) ? d : 0][slot];
   if (b.cap < bytes) {
     if (b.p) cudaFree(b.p);
     b.p = nullptr;
@@ -137,13 +143,20 @@ static const RegsFn k_tthreads[17] = NID_TABLE(track_threads_);
 // the same GPU as the workspaces and handles.
 #define BIND()                                                        \
   do {                                                                \
-    if (g_device >= 0) {                                              \
-      cudaError_t be_ = cudaSetDevice(g_device);                      \
+    if (cur_device() >= 0) {                                          \
+      cudaError_t be_ = cudaSetDevice(cur_device());                  \
       if (be_ != cudaSuccess) {                                       \
         g_err = std::string("cudaSetDevice: ") + cudaGetErrorString(be_); \
         return 2;                                                     \
       }                                                               \
     }                                                                 \
+  } while (0)
+
+// entry points that take a handle run on the handle's device
+#define BIND_H(h)                                            \
+  do {                                                       \
+    if ((h) && (h)->device >= 0) t_device = (h)->device;     \
+    BIND();                                                  \
   } while (0)
 
 // CUDA events destroyed on every exit path
@@ -190,12 +203,55 @@ int nid_init(int device) {
 }
 
 int nid_shutdown(void) {
-  BIND();
-  for (auto& b : g_bufs) {
-    if (b.p) cudaFree(b.p);
-    b.p = nullptr;
-    b.cap = 0;
+  for (int d = 0; d < 16; ++d) {
+    bool any = false;
+    for (auto& b : g_bufs[d]) any = any || b.p;
+    if (!any) continue;
+    CK(cudaSetDevice(d));
+    for (auto& b : g_bufs[d]) {
+      if (b.p) cudaFree(b.p);
+      b.p = nullptr;
+      b.cap = 0;
+    }
   }
+  BIND();
+  return 0;
+}
+
+int nid_init_devices(int ndev, const int* devs) {
+  if (ndev < 1 || ndev > 16 || !devs) FAIL("nid_init_devices: 1..16 devices");
+  int have = 0;
+  CK(cudaGetDeviceCount(&have));
+  for (int i = 0; i < ndev; ++i)
+    if (devs[i] < 0 || devs[i] >= have || devs[i] >= 16) FAIL("nid_init_devices: no such device");
+  for (int i = 0; i < ndev; ++i) {
+    CK(cudaSetDevice(devs[i]));
+    CK(cudaFree(0));
+    g_devs[i] = devs[i];
+    // peer access for the endpoint gather (NVLink / NVSwitch P2P); already-enabled is fine
+    for (int j = 0; j < ndev; ++j) {
+      if (devs[j] == devs[i]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devs[i], devs[j]);
+      if (can) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(devs[j], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+        cudaGetLastError();
+      }
+    }
+  }
+  g_ndev = ndev;
+  g_device = devs[0];
+  t_device = devs[0];
+  CK(cudaSetDevice(devs[0]));
+  return 0;
+}
+
+int nid_use_device(int i) {
+  if (g_ndev == 0) FAIL("nid_use_device: call nid_init_devices first");
+  if (i < 0 || i >= g_ndev) FAIL("nid_use_device: index out of range");
+  t_device = g_devs[i];
+  CK(cudaSetDevice(t_device));
   return 0;
 }
 
@@ -210,6 +266,8 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   if (d->n < 1 || d->n > NID_MAX_VARS) FAIL("n must be in 1..16");
   if (d->nterms < 0) FAIL("negative term count");
   const int n = d->n, T = d->nterms;
+  int here_ = 0;
+  CK(cudaGetDevice(&here_));
   std::vector<int> off(d->row_off, d->row_off + n + 1);
   if (off[0] != 0 || off[n] != T) FAIL("row offsets do not cover the term table");
   for (int i = 0; i < n; ++i)
@@ -242,6 +300,7 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
       if (d->coef_start[k] != 0.0) FAIL("total-degree start: the term table must hold only the target");
   }
   NidHomotopy* h = new NidHomotopy();
+  h->device = here_;
   h->n = n;
   h->nterms = T;
   h->nparam = d->nparam;
@@ -500,7 +559,7 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
 
 int nid_homotopy_destroy(NidHomotopy* h) {
   if (!h) return 0;
-  BIND();
+  BIND_H(h);
   cudaFree(h->row_off);
   cudaFree(h->expo);
   delete h->ptab;
@@ -535,7 +594,7 @@ int nid_last_counters(NidCounters* c) {
 // slot map for the workspace cache
 enum {
   W_STARTS = 0, W_PARAMS, W_XEND, W_STATUS, W_STEPS, W_TREACH, W_RESID, W_COND, W_REG,
-  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS, W_GSTATE, W_PTW, W_TRACE, W_TRACEN
+  W_COUNT, W_SCR, W_DDSCR, W_X, W_T, W_H, W_J, W_SCALE, W_I32, W_I8, W_I8B, W_TOL, W_ROOTS, W_GSTATE, W_PTW, W_TRACE, W_TRACEN, W_CBLK, W_COFF, W_GBUF, W_GIDX
 };
 
 static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const double* starts, long long first_index,
@@ -584,7 +643,7 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
     FAIL("double-double tracking and step traces are not available for per-cell polyhedral homotopies");
   if (trace_cap > 0 && (!trace || !trace_n)) FAIL("trace buffers missing");
   if (trace_cap > 0 && device_io) FAIL("step traces are returned to host buffers only");
-  BIND();
+  BIND_H(h);
   if (index_stride < 1) FAIL("index_stride must be >= 1");
   if (P < 0) FAIL("negative path count");
   const int n = h->n;
@@ -795,7 +854,7 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
 int nid_eval_batch(NidHomotopy* h, int P, const double* x, const double* t, const double* params, int param_div,
                    double* H, double* J, double* scale) {
   if (!h || !x || !t || !H || !J || !scale) FAIL("null argument");
-  BIND();
+  BIND_H(h);
   if (P <= 0) return 0;
   const int n = h->n;
   if (param_div < 1) param_div = 1;
@@ -877,7 +936,7 @@ int nid_refine_batch(NidHomotopy* h, int P, double* x, double tol, int iters, in
                      double infinity_threshold, double* residual, double* condition, int8_t* regular,
                      int32_t* rank, int8_t* slack_class) {
   if (!h || !x || !residual || !condition || !regular || !rank || !slack_class) FAIL("null argument");
-  BIND();
+  BIND_H(h);
   if (h->nparam > 0) FAIL("refine does not take per-path parameters");
   if (P <= 0) return 0;
   const int n = h->n;
@@ -918,7 +977,7 @@ int nid_refine_batch(NidHomotopy* h, int P, double* x, double tol, int iters, in
 
 int nid_dd_refine_batch(NidHomotopy* h, int P, double* x, int steps, int8_t* ok) {
   if (!h || !x || !ok) FAIL("null argument");
-  BIND();
+  BIND_H(h);
   if (h->nparam > 0) FAIL("dd refine does not take per-path parameters");
   if (P <= 0) return 0;
   const int n = h->n;
@@ -965,6 +1024,108 @@ int nid_match_pairs(int n, int ncmp, int P, const double* X, int32_t* pairs, lon
   long long k = (long long)c < max_pairs ? (long long)c : max_pairs;
   if (k > 0 && pairs) CK(cudaMemcpy(pairs, dp, (size_t)k * 2 * sizeof(int), cudaMemcpyDeviceToHost));
   return 0;
+}
+
+// K7 pre-pass on the current device: succeeded endpoints of one shard,
+// compacted in path order (device pointers in and out)
+static int compact_finite(int n, long long P, const cd* x, const int8_t* status, long long first_index,
+                          long long index_stride, cd* out, long long* index_out, long long capacity, long long* count,
+                          cudaStream_t s) {
+  *count = 0;
+  if (P <= 0) return 0;
+  const int nb = (int)((P + 255) / 256);
+  int* d_cnt = ws<int>(W_CBLK, nb);
+  long long* d_off = ws<long long>(W_COFF, nb);
+  if (!d_cnt || !d_off) FAIL("out of device memory (compaction)");
+  finite_count_kernel<<<nb, 256, 0, s>>>(P, status, d_cnt);
+  CK(cudaGetLastError());
+  std::vector<int> hc(nb);
+  CK(cudaMemcpyAsync(hc.data(), d_cnt, nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<long long> ho(nb);
+  long long tot = 0;
+  for (int b = 0; b < nb; ++b) {
+    ho[b] = tot;
+    tot += hc[b];
+  }
+  *count = tot;
+  if (tot > capacity) FAIL("compaction: output capacity too small");
+  if (tot == 0) return 0;
+  CK(cudaMemcpyAsync(d_off, ho.data(), nb * sizeof(long long), cudaMemcpyHostToDevice, s));
+  finite_compact_kernel<<<nb, 256, 0, s>>>(P, n, x, status, d_off, first_index, index_stride, out, index_out);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int nid_compact_finite(int n, long long P, const double* x_end, const int8_t* status, long long first_index,
+                       long long index_stride, double* x_out, long long* index_out, long long capacity,
+                       long long* count, void* stream) {
+  if (n < 1 || n > NID_MAX_VARS || !x_end || !status || !x_out || !count) FAIL("bad argument");
+  BIND();
+  return compact_finite(n, P, (const cd*)x_end, status, first_index, index_stride, (cd*)x_out, index_out, capacity,
+                        count, (cudaStream_t)stream);
+}
+
+int nid_gather_endpoints(int nparts, const int* part_device, const double* const* x_end, const int8_t* const* status,
+                         const long long* counts, const long long* first_index, const long long* index_stride, int n,
+                         int root_device, double* x_out, long long* index_out, long long capacity, long long* total) {
+  if (g_ndev == 0) FAIL("nid_gather_endpoints: call nid_init_devices first");
+  if (nparts < 1 || !part_device || !x_end || !status || !counts || !x_out || !total) FAIL("bad argument");
+  if (n < 1 || n > NID_MAX_VARS) FAIL("n must be in 1..16");
+  if (root_device < 0 || root_device >= g_ndev) FAIL("root device index out of range");
+  const int saved = t_device;
+  const int root = g_devs[root_device];
+  long long off = 0;
+  int rc = 0;
+  for (int p = 0; p < nparts && rc == 0; ++p) {
+    if (part_device[p] < 0 || part_device[p] >= g_ndev) {
+      g_err = "part device index out of range";
+      rc = 1;
+      break;
+    }
+    const int dev = g_devs[part_device[p]];
+    t_device = dev;
+    cudaError_t e = cudaSetDevice(dev);
+    if (e != cudaSuccess) {
+      g_err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+      rc = 2;
+      break;
+    }
+    const long long P = counts[p];
+    cd* buf = ws<cd>(W_GBUF, (size_t)(P > 0 ? P : 1) * n);
+    long long* ibuf = index_out ? ws<long long>(W_GIDX, (size_t)(P > 0 ? P : 1)) : nullptr;
+    if (!buf || (index_out && !ibuf)) {
+      g_err = "out of device memory (gather staging)";
+      rc = 1;
+      break;
+    }
+    long long cnt = 0;
+    rc = compact_finite(n, P, (const cd*)x_end[p], status[p], first_index ? first_index[p] : 0,
+                        index_stride ? index_stride[p] : 1, buf, ibuf, P, &cnt, 0);
+    if (rc) break;
+    if (off + cnt > capacity) {
+      g_err = "nid_gather_endpoints: output capacity too small";
+      rc = 1;
+      break;
+    }
+    if (cnt > 0) {
+      // device-to-device over NVLink when the part lives on another GPU
+      e = cudaMemcpyPeer((cd*)x_out + off * n, root, buf, dev, (size_t)cnt * n * sizeof(cd));
+      if (e == cudaSuccess && index_out)
+        e = cudaMemcpyPeer(index_out + off, root, ibuf, dev, (size_t)cnt * sizeof(long long));
+      if (e != cudaSuccess) {
+        g_err = std::string("cudaMemcpyPeer: ") + cudaGetErrorString(e);
+        rc = 2;
+        break;
+      }
+    }
+    off += cnt;
+  }
+  *total = off;
+  t_device = saved;
+  if (cur_device() >= 0) cudaSetDevice(cur_device());
+  return rc;
 }
 
 }  // extern "C"
