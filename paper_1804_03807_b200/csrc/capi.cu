@@ -757,11 +757,11 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   a.scratch = ws<cd>(W_SCR, (size_t)max_blocks * k_tthreads[n]() * (3 * n * n + 2 * n));
   if (!a.scratch) FAIL("out of device memory (scratch)");
   a.gstate = ws<cd>(W_GSTATE, (size_t)max_blocks * 3 * n * rows::SLOTS);
-  // per-slot evaluation of long paths (streamed-record tracker, n >= 8): in a
-  // small launch the slowest paths set the launch time, so a path switches
-  // after lat_steps steps; in a large one only far outliers do
-  a.lat_steps = P <= 16384 ? 64 : 512;
-  if (getenv("NID_LAT_STEPS")) a.lat_steps = atoi(getenv("NID_LAT_STEPS"));
+  // per-slot evaluation (streamed-record tracker, n >= 8) when a block has at
+  // most lat_slots evaluating slots: the drain of a launch and launches smaller
+  // than the machine, where a level lasts as long as its slowest paths
+  a.lat_slots = 8;
+  if (getenv("NID_LAT_SLOTS")) a.lat_slots = atoi(getenv("NID_LAT_SLOTS"));
   if (!a.gstate) FAIL("out of device memory (slot state)");
 
   double* d_trace = nullptr;

@@ -20,43 +20,59 @@
 // term with repeated products in variable order (polynomials.py:293-314).
 template <int N>
 NID_D void cdd_row(const HomDev& H, int row, const cdd (&x)[N], const cd* prm, cdd& rv, cdd* Jrow) {
+  // One prefix and one suffix pass over each term's variables give the value
+  // and every partial derivative (the reference multiplies each derivative
+  // term out on its own, polynomials.py:293-314: the same products, other
+  // association, a double-double rounding apart).
   rv = cdd_zero();
   if (row >= H.n) return;
   const int k0 = H.row_off[row], k1 = H.row_off[row + 1];
+  cdd Jr[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) Jr[j] = cdd_zero();
+  const cdd one = cdd_from(cd{1.0, 0.0});
+#pragma unroll 1
   for (int k = k0; k < k1; ++k) {
     cd c = H.ct[k];
     if (H.pslot != nullptr && H.pslot[k] >= 0) c = prm[H.pslot[k]];
     if (c.re == 0.0 && c.im == 0.0) continue;
-    uint4 ew = H.expo[k];
+    const uint4 ew = H.expo[k];
     const unsigned w[4] = {ew.x, ew.y, ew.z, ew.w};
-    cdd v = cdd_from(c);
-#pragma unroll
+    cdd F[N], D[N], P[N];
+    int var[N];
+    int K = 0;
+#pragma unroll 1
     for (int u = 0; u < N; ++u) {
-      int a = expo_at(w, u);
-      for (int e = 0; e < a; ++e) v = cdd_mul(v, x[u]);
+      const int a = expo_at(w, u);
+      if (a == 0) continue;
+      cdd pw = one;
+      for (int e = 1; e < a; ++e) pw = cdd_mul(pw, x[u]);
+      F[K] = a == 1 ? x[u] : cdd_mul(pw, x[u]);
+      const dd aa = dd{(double)a, 0.0};
+      D[K] = a == 1 ? pw : cdd{dd_mul(pw.re, aa), dd_mul(pw.im, aa)};
+      var[K] = u;
+      ++K;
     }
-    rv = cdd_add(rv, v);
-  }
-  for (int j = 0; j < N; ++j) {
-    cdd acc = cdd_zero();
-    for (int k = k0; k < k1; ++k) {
-      uint4 ew = H.expo[k];
-      const unsigned w[4] = {ew.x, ew.y, ew.z, ew.w};
-      int aj = expo_at(w, j);
-      if (aj == 0) continue;
-      cd c = H.ct[k];
-      if (H.pslot != nullptr && H.pslot[k] >= 0) c = prm[H.pslot[k]];
-      if (c.re == 0.0 && c.im == 0.0) continue;
-      cdd v = cdd_from(cd{c.re * aj, c.im * aj});
+    cdd p = cdd_from(c);
+#pragma unroll 1
+    for (int q = 0; q < K; ++q) {
+      P[q] = p;
+      p = cdd_mul(p, F[q]);
+    }
+    rv = cdd_add(rv, p);
+    cdd sfx = one;
+#pragma unroll 1
+    for (int q = K - 1; q >= 0; --q) {
+      const cdd d = cdd_mul(cdd_mul(P[q], D[q]), sfx);
+      const int u = var[q];
 #pragma unroll
-      for (int u = 0; u < N; ++u) {
-        int a = expo_at(w, u) - (u == j ? 1 : 0);
-        for (int e = 0; e < a; ++e) v = cdd_mul(v, x[u]);
-      }
-      acc = cdd_add(acc, v);
+      for (int j = 0; j < N; ++j)
+        if (j == u) Jr[j] = cdd_add(Jr[j], d);
+      sfx = cdd_mul(sfx, F[q]);
     }
-    Jrow[j] = acc;
   }
+#pragma unroll
+  for (int j = 0; j < N; ++j) Jrow[j] = Jr[j];
 }
 
 // per-group double-double scratch layout (cdd units)
@@ -108,54 +124,56 @@ NID_D bool dd_polish(const Grp<N>& g, const HomDev& H, const cd* prm, const cd (
     }
     __syncwarp(g.mask);
     int stop = 0;
+    double scale = 0.0;
     if (g.lg == 0) {
-      double scale = 0.0;
       for (int i = 0; i < N; ++i) scale = fmax(scale, cdd_abs(As[i * (N + 1) + i]));
       if (scale == 0.0) scale = 1.0;
       const double lam = 1e-26 * scale;
       for (int i = 0; i < N; ++i) As[i * (N + 1) + i] = cdd_add_real(As[i * (N + 1) + i], lam);
-      // solve_dd: Gaussian elimination, partial pivoting on |.| (linalg.py:54-76)
-      for (int k = 0; k < N && !fail; ++k) {
-        int piv = k;
-        double best = cdd_abs(As[k * (N + 1) + k]);
-        for (int i = k + 1; i < N; ++i) {
-          double a = cdd_abs(As[i * (N + 1) + k]);
-          if (a > best) {
-            best = a;
-            piv = i;
-          }
+    }
+    __syncwarp(g.mask);
+    // solve_dd: Gaussian elimination, partial pivoting on |.| (linalg.py:54-76),
+    // lane i eliminating row i (the same operations per entry as the serial
+    // loop); the pivot is the first largest |A_ik|, i >= k
+    for (int k = 0; k < N && !fail; ++k) {
+      double a = g.lg >= k ? cdd_abs(As[g.lg * (N + 1) + k]) : -1.0;
+      if (!(a == a)) a = -1.0;
+      const double best = group_reduce<N>(g, a, OpMax());
+      const unsigned eq = (__ballot_sync(g.mask, g.lg >= k && a == best) & g.bits) >> g.gbase;
+      const int piv = eq ? __ffs(eq) - 1 : k;
+      if (!(best > 0.0)) {
+        fail = 1;
+        break;
+      }
+      if (piv != k) {
+        for (int j = g.lg; j <= N; j += N) {
+          const cdd tmp = As[k * (N + 1) + j];
+          As[k * (N + 1) + j] = As[piv * (N + 1) + j];
+          As[piv * (N + 1) + j] = tmp;
         }
-        if (best == 0.0) {
-          fail = 1;
-          break;
-        }
-        if (piv != k)
-          for (int j = 0; j <= N; ++j) {
-            cdd tmp = As[k * (N + 1) + j];
-            As[k * (N + 1) + j] = As[piv * (N + 1) + j];
-            As[piv * (N + 1) + j] = tmp;
-          }
-        cdd inv = As[k * (N + 1) + k];
-        for (int i = k + 1; i < N; ++i) {
-          cdd f = cdd_div(As[i * (N + 1) + k], inv);
-          if (f.re.hi == 0.0 && f.im.hi == 0.0) continue;
+      }
+      __syncwarp(g.mask);
+      if (g.lg > k) {
+        const int i = g.lg;
+        const cdd f = cdd_div(As[i * (N + 1) + k], As[k * (N + 1) + k]);
+        if (!(f.re.hi == 0.0 && f.im.hi == 0.0))
           for (int j = k; j <= N; ++j)
             As[i * (N + 1) + j] = cdd_sub(As[i * (N + 1) + j], cdd_mul(f, As[k * (N + 1) + j]));
-        }
       }
-      if (!fail) {
-        for (int k = N - 1; k >= 0; --k) {
-          cdd s = As[k * (N + 1) + N];
-          for (int j = k + 1; j < N; ++j) s = cdd_sub(s, cdd_mul(As[k * (N + 1) + j], Ds[j]));
-          Ds[k] = cdd_div(s, As[k * (N + 1) + k]);
-        }
-        double mx = 0.0;
-        for (int v = 0; v < N; ++v) {
-          Ps[v] = cdd_add(Ps[v], Ds[v]);
-          mx = fmax(mx, cdd_abs(Ds[v]));
-        }
-        if (mx < 1e-14 * scale) stop = 1;
+      __syncwarp(g.mask);
+    }
+    if (g.lg == 0 && !fail) {
+      for (int k = N - 1; k >= 0; --k) {
+        cdd s = As[k * (N + 1) + N];
+        for (int j = k + 1; j < N; ++j) s = cdd_sub(s, cdd_mul(As[k * (N + 1) + j], Ds[j]));
+        Ds[k] = cdd_div(s, As[k * (N + 1) + k]);
       }
+      double mx = 0.0;
+      for (int v = 0; v < N; ++v) {
+        Ps[v] = cdd_add(Ps[v], Ds[v]);
+        mx = fmax(mx, cdd_abs(Ds[v]));
+      }
+      if (mx < 1e-14 * scale) stop = 1;
     }
     fail = __shfl_sync(g.mask, fail, g.gbase);
     stop = __shfl_sync(g.mask, stop, g.gbase);

@@ -114,6 +114,12 @@ NID_D void eval_row(const HomDev& H, int row, const cd (&x)[N], double t, const 
   }
   const bool ml = H.multilinear != 0;
   const int maxdeg = H.maxdeg;
+  cd xl[N], Jl[N];
+#pragma unroll
+  for (int v = 0; v < N; ++v) {
+    xl[v] = x[v];
+    Jl[v] = cd{0.0, 0.0};
+  }
   for (int k = k0; k < k1; ++k) {
     uint4 ew = __ldg(H.expo + k);
     const unsigned w[4] = {ew.x, ew.y, ew.z, ew.w};
@@ -143,24 +149,43 @@ NID_D void eval_row(const HomDev& H, int row, const cd (&x)[N], double t, const 
         s = csel(on, s * x[v], s);
       }
     } else {
-#pragma unroll
-      for (int v = 0; v < N; ++v) {
-        P[v] = p;
-        cd f, d;
-        cpow_pair(x[v], expo_at(w, v), maxdeg, f, d);
-        p = p * f;
+      // factor list of the term (its variables ascending, with exponents):
+      // the same products in the same order as the variable-by-variable sweep
+      // (absent variables multiply by one), without its N-wide predicated work.
+      // xl / Jl are indexed per lane (lanes walk different rows): local memory.
+      const uint4 fl = __ldg(H.fac + k);
+      const uint4 fe = __ldg(H.fex + k);
+      const int K = (int)fl.z;
+      cd F[N], D[N];
+#pragma unroll 1
+      for (int q = 0; q < K; ++q) {
+        const int v = ((q < 8 ? fl.x : fl.y) >> (4 * (q & 7))) & 15;
+        const int a = ((q < 4 ? fe.x : (q < 8 ? fe.y : (q < 12 ? fe.z : fe.w))) >> (8 * (q & 3))) & 255;
+        const cd xv = xl[v];
+        cd pw = xv, prev = cd{1.0, 0.0};
+#pragma unroll 1
+        for (int e = 2; e <= a; ++e) {
+          prev = pw;
+          pw = pw * xv;
+        }
+        P[q] = p;
+        F[q] = pw;
+        D[q] = (double)a * prev;
+        p = p * pw;
       }
       hv = cfma(c, p, hv);
       cd s = cd{1.0, 0.0};
-#pragma unroll
-      for (int v = N - 1; v >= 0; --v) {
-        const int a = expo_at(w, v);
-        cd f, d;
-        cpow_pair(x[v], a, maxdeg, f, d);
-        J[v] = csel(a != 0, cfma(P[v] * s, c * d, J[v]), J[v]);
-        s = s * f;
+#pragma unroll 1
+      for (int q = K - 1; q >= 0; --q) {
+        const int v = ((q < 8 ? fl.x : fl.y) >> (4 * (q & 7))) & 15;
+        Jl[v] = cfma(P[q] * s, c * D[q], Jl[v]);
+        s = s * F[q];
       }
     }
+  }
+  if (!ml) {
+#pragma unroll
+    for (int v = 0; v < N; ++v) J[v] = Jl[v];
   }
   // total-degree start row: G_i = x_i^{d_i} - 1, dG_i/dx_i = d_i x_i^{d_i - 1}
   double xa_td = 0.0;

@@ -26,7 +26,7 @@ struct TrackArgs {
   unsigned long long* counters;  // evals, jacs, scales, lstsq fallbacks
   cd* scratch;                   // per-group lstsq scratch, 3*n*n + 2*n complex each
   cd* gstate;                    // per-slot accepted/previous point, DN direction [block][3n][32]
-  int lat_steps;                 // a path past this many steps is evaluated per slot (track_rec.cuh)
+  int lat_slots;                 // per-slot evaluation when at most this many of a block's slots evaluate (track_rec.cuh)
   // per-step trace of accepted steps (auxiliary kernel only, track_aux.cuh):
   // (t, step, corrector iterations) rows [P][trace_cap][3], counts [P]; null: off
   double* trace;

@@ -53,7 +53,7 @@ enum IField {
   I_ACT, I_MODE, I_CTX, I_CITERS, I_CIT, I_CPHASE, I_CITS, I_DNIT, I_DNTRIAL, I_USED, I_OUTST, I_FLAGS, I_BAD,
   I_COUNT
 };
-enum Flag { F_COK = 1, F_HAVEPREV = 2, F_ENDGAME = 4, F_NEEDSCALE = 8, F_HASX = 16, F_FALLBACK = 32, F_LAT = 64 };
+enum Flag { F_COK = 1, F_HAVEPREV = 2, F_ENDGAME = 4, F_NEEDSCALE = 8, F_HASX = 16, F_FALLBACK = 32 };
 
 template <int N>
 struct Lay {
@@ -533,7 +533,6 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
           continue;
         }
         IS_(I_USED) += 1;
-        if (IS_(I_USED) > Ar.lat_steps) SETF(F_LAT, true);  // per-slot evaluation from now on
         double hs = fmin(fmin(DS_(D_STEP), q.max_step), rem);
         if (HAS(F_ENDGAME)) hs = fmin(hs, q.endgame_contraction * rem);
         double tt = t + hs;
@@ -754,7 +753,13 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     if constexpr (rec_on<N>() && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value) {
       if (Ar.H.rec) {  // streamed records: every lane of the warp takes part
         const bool act0 = W_IS(I_ACT) == A_EVAL;
-        const bool lat = lat_on<N>() && act0 && (W_IS(I_FLAGS) & F_LAT) != 0;
+        // Few evaluating slots in the block (the tail of a launch, or a launch
+        // smaller than the machine): the row-per-warp pass would run with most
+        // lanes idle, so each slot is evaluated on its own with its rows' terms
+        // split over the warp's 32 lanes.  Every warp sees the same 32 slots,
+        // so the decision is block-uniform without a barrier.
+        const int nact = __popc(__ballot_sync(0xffffffffu, act0));  // (every lane votes: no short circuit)
+        const bool lat = lat_on<N>() && act0 && nact <= Ar.lat_slots;
         const bool act = act0 && !lat;  // slots of the row-per-warp pass
         const bool want = act && (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
         const long long pr = lb[S + lane];
@@ -763,7 +768,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
         if (__any_sync(0xffffffffu, act))
           eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
                            db + L::AXW * S + lane, ring);
-        // paths past lat_steps steps: one slot at a time, the warp's lanes split the terms
+        // few evaluating slots: one slot at a time, the warp's lanes split the terms
         unsigned lm = __ballot_sync(0xffffffffu, lat);
         unsigned char* scr = smem_ctl + L::bytes() + ring_bytes<N>() + (size_t)g * lat::warp_bytes<N>();
 #pragma unroll 1

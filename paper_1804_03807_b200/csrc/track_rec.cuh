@@ -272,8 +272,8 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
 // block iteration lasts as long as a warp's walk over its rows' terms (~500
 // for C3's heavy rows) whether 32 slots are active or one.  In the tail of a
 // small launch (a cascade level of ~5k paths whose slowest path takes 30x the
-// mean number of steps) almost every slot is idle, so a path that has taken
-// more than TrackArgs::lat_steps steps is evaluated here instead: the warp's
+// mean number of steps) almost every slot is idle, so when at most
+// TrackArgs::lat_slots of the block's slots evaluate, each is evaluated here instead: the warp's
 // 32 lanes split its rows' terms (lane l takes records l, l+32, ...), each
 // lane accumulates into its own row of a per-warp shared-memory scratch, and
 // the rows are summed in lane order.  The term arithmetic is t_load /
@@ -354,8 +354,10 @@ NID_D void lane_terms(const TermRec* recs, long long r, long long r1, const cd* 
 // The rows of warp group g for ONE slot s (warp-uniform), every lane taking
 // part.  xs / axs / aug / dbl: the block's arrays at slot s (stride SLOTS);
 // scr: this warp's lat::warp_bytes<N>() of shared memory.
+// Out of line: its registers are allocated apart from the block loop's (inlined, it
+// pushed the n = 14 kernel into 1.1 KB of spills and cost the row-per-warp pass 14 %).
 template <int N>
-NID_D void eval_slot_rec(const HomDev& H, int g, const cd* xs, double t, const cd* prm, cd* aug, double* dbl, bool ws,
+__device__ __noinline__ void eval_slot_rec(const HomDev& H, int g, const cd* xs, double t, const cd* prm, cd* aug, double* dbl, bool ws,
                          const double* axs, unsigned char* scr) {
   using L = rows::Layout<N>;
   constexpr int S = rows::SLOTS;
