@@ -17,8 +17,9 @@
 #include "track_ctl.cuh"
 
 static thread_local std::string g_err;
-static NidCounters g_counters = {};
-static unsigned long long g_phase[7] = {};
+// per host thread: one thread per device may track concurrently (nid_init_devices)
+static thread_local NidCounters g_counters = {};
+static thread_local unsigned long long g_phase[7] = {};
 static int g_device = -1;          // the process default (nid_init)
 static thread_local int t_device = -1;  // this host thread's choice (nid_use_device / a handle's device)
 static int g_devs[16];
