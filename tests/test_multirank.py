@@ -169,3 +169,29 @@ def test_group_shard_and_on_root_single_rank():
     assert parallel.on_root(lambda a, b: a + b, 2, 3) == 5
     with pytest.raises(ValueError):
         parallel.shard_strided(10, 3, 3)
+
+
+def test_torchrun_two_ranks_gloo():
+    """The launch line of the driver (`python -m torch.distributed.run --nnodes=1
+    --nproc-per-node 2 --master-addr 127.0.0.1 --master-port P ...`) on CPU / gloo:
+    both shapes of the multi-rank path (per-rank shard + gather to rank 0, and the
+    sharded stage driver) agree with the one-rank records."""
+    import json
+    import subprocess
+    import sys
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(here, "mr_torchrun_worker.py")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    p2 = configs.c2()
+    one = oracle_track_local(LinearHomotopy(p2.start, p2.target, p2.gamma), None, degrees=p2.degrees, count=48)
+    assert line["world"] == 2 and line["max"] == 2.0
+    assert line["finite"] == line["gathered"] == line["full_finite"] == int(one.succeeded.sum())
+    assert line["full_paths"] == 48 and line["status"] == one.status.tolist()
