@@ -113,6 +113,32 @@ class DistContext:
             dist.destroy_process_group()
 
 
+def compact_finite(x_end, status):
+    """The succeeded endpoints of a shard in path order: on a CUDA tensor the
+    library's own compaction kernels (nid_compact_finite, the K7 pre-pass of
+    SURVEY §2.2), on a CPU tensor (gloo tests) a boolean mask."""
+    import torch
+
+    if not x_end.is_cuda:
+        return x_end[(status == 0) | (status == 2)]
+    import ctypes as C
+
+    from . import _lib
+
+    P = int(status.shape[0])
+    if P == 0:
+        return x_end[:0]
+    L = _lib.lib()
+    n = int(x_end.shape[1])
+    x_end = x_end.contiguous()
+    out = torch.empty_like(x_end)
+    cnt = C.c_longlong(0)
+    stream = torch.cuda.current_stream().cuda_stream
+    _lib.check(L.nid_compact_finite(n, P, C.c_void_p(x_end.data_ptr()), C.c_void_p(status.data_ptr()), 0, 1,
+                                    C.c_void_p(out.data_ptr()), None, P, C.byref(cnt), C.c_void_p(stream or None)), L)
+    return out[: cnt.value]
+
+
 def gather_finite(ctx: DistContext, x_end, status):
     """Compact this rank's succeeded endpoints (status converged/singular)
     and gather them to rank 0: all_gather of counts, then an all_gather of
@@ -121,8 +147,7 @@ def gather_finite(ctx: DistContext, x_end, status):
     import torch
     import torch.distributed as dist
 
-    mask = (status == 0) | (status == 2)
-    pts = x_end[mask]
+    pts = compact_finite(x_end, status)
     if ctx.world == 1:
         return pts
     cnt = torch.tensor([pts.shape[0]], dtype=torch.int64, device=pts.device)

@@ -100,3 +100,24 @@ def test_empty_shard_and_all_failed(nid):
     _lib.check(L.nid_compact_finite(n, 0, C.c_void_p(x.data_ptr()), C.c_void_p(st.data_ptr()), 0, 1,
                                     C.c_void_p(out.data_ptr()), None, 5, C.byref(cnt), None), L)
     assert cnt.value == 0
+
+
+def test_compact_finite_tensor_path(nid):
+    """parallel.compact_finite on CUDA tensors (what bench.py's endpoint gather
+    uses) equals the boolean-mask compaction, for shapes [P, n, 2]."""
+    import torch
+
+    from paper_1804_03807_b200 import parallel
+
+    g = torch.Generator(device="cpu").manual_seed(3)
+    for P in (0, 1, 255, 256, 257, 5000):
+        x = torch.randn((P, 7, 2), generator=g, dtype=torch.float64)
+        st = torch.randint(0, 4, (P,), generator=g, dtype=torch.int8)
+        want = x[(st == 0) | (st == 2)]
+        got = parallel.compact_finite(x.cuda(), st.cuda())
+        assert got.shape == want.shape and torch.equal(got.cpu(), want)
+        assert torch.equal(parallel.compact_finite(x, st), want)
+    ctx = parallel.DistContext()
+    x = torch.randn((100, 4, 2), generator=g, dtype=torch.float64).cuda()
+    st = torch.randint(0, 4, (100,), generator=g, dtype=torch.int8).cuda()
+    assert torch.equal(parallel.gather_finite(ctx, x, st), x[(st == 0) | (st == 2)])
