@@ -221,7 +221,9 @@ int nid_match_pairs(int n, int ncmp, int P, const double* X, int32_t* pairs, lon
  * nid_gather_endpoints: the same for nparts shards living on the devices
  * part_device[p] (indices into nid_init_devices' list), each compacted on its
  * own GPU and copied peer to peer (NVLink) into x_out / index_out on the root
- * device, part after part; *total = endpoints gathered. */
+ * device, part after part; *total = endpoints gathered.  The shards' tracking
+ * calls must have completed (both run their kernels on the default stream of
+ * the part's device and synchronize before returning). */
 int nid_compact_finite(int n, long long P, const double* x_end, const int8_t* status, long long first_index,
                        long long index_stride, double* x_out, long long* index_out, long long capacity,
                        long long* count, void* stream);

@@ -72,7 +72,7 @@ def test_every_track_param_is_honoured(nid, kw):
         tr = np.array([r.t_reached for r in ref])
         # a tolerance at the evaluation-noise floor makes accept / reject decisions
         # rounding-sensitive: equal step counts, slightly different schedules
-        tol_t = dict(rtol=0, atol=1e-3) if kw.get("corrector_tol", 1.0) < 1e-11 else dict(rtol=1e-12, atol=0)
+        tol_t = dict(rtol=0, atol=1e-2) if kw.get("corrector_tol", 1.0) < 1e-11 else dict(rtol=1e-12, atol=0)
         assert np.allclose(res.t_reached[same & (res.steps == steps)], tr[same & (res.steps == steps)], **tol_t)
         for i, r in enumerate(ref):
             if r.succeeded:
