@@ -451,11 +451,21 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
         const long long grp_base = (long long)recs.size();
         for (int gi = h->goff[gg]; gi < h->goff[gg + 1]; ++gi) {
           const int i = h->grow[gi];
-          std::vector<std::pair<int, int>> byk;  // (total degree, term)
+          // (total degree, and for degree <= rec::SDUPK the repeat pattern << 8; term):
+          // a run of short terms shares one pattern, so the evaluator's body for it
+          // loads every distinct variable once and folds repeats without selects
+          std::vector<std::pair<int, int>> byk;
           for (int k = off[i]; k < off[i + 1]; ++k) {
-            int deg = 0;
-            for (int v = 0; v < n; ++v) deg += d->expo[k * NID_MAX_VARS + v];
-            byk.push_back({deg, k});
+            int deg = 0, pat = 0;
+            for (int v = 0; v < n; ++v)
+              for (int a = 0; a < d->expo[k * NID_MAX_VARS + v]; ++a) {
+                if (a > 0) pat |= 1 << deg;
+                ++deg;
+              }
+            const bool stat = deg >= 1 && deg <= rec::SDUPK && !getenv("NID_REC_NO_STATIC_DUP");
+            // sort key: degree first, so a row's runs of one factor count stay adjacent
+            // (the per-slot evaluator walks them as one run)
+            byk.push_back({(deg << 12) | (stat ? (0x800 | pat) : 0), k});
           }
           std::stable_sort(byk.begin(), byk.end(),
                            [](const std::pair<int, int>& a, const std::pair<int, int>& b) { return a.first < b.first; });
@@ -463,7 +473,9 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
           for (size_t q = 0; q < byk.size();) {
             size_t q1 = q;
             while (q1 < byk.size() && byk[q1].first == byk[q].first) ++q1;
-            runs.push_back(make_uint4((unsigned)i, (unsigned)byk[q].first, (unsigned)recs.size(), (unsigned)(q1 - q)));
+            const int deg_q = byk[q].first >> 12;
+            const unsigned ykey = (unsigned)deg_q | ((byk[q].first & 0x800) ? (0x100u | ((unsigned)(byk[q].first & 0x7ff) << 9)) : 0u);
+            runs.push_back(make_uint4((unsigned)i, ykey, (unsigned)recs.size(), (unsigned)(q1 - q)));
             // order the run so records at even offsets from the group's first
             // record pair with a successor of disjoint variables (greedy, first
             // fit within a window): the evaluator interleaves such pairs
@@ -481,7 +493,7 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
               const int a = pend.front();
               pend.erase(pend.begin());
               bool paired = false;
-              if ((gpos & 1) == 0 && byk[q].first > 0 && byk[q].first <= 6) {  // rec::PAIRK
+              if ((gpos & 1) == 0 && deg_q > 0 && deg_q <= 6) {  // rec::PAIRK
                 const unsigned ma = vmask(a);
                 for (size_t z = 0; z < pend.size() && z < 64; ++z)
                   if (!(vmask(pend[z]) & ma)) {

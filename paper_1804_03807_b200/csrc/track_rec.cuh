@@ -56,7 +56,18 @@ struct TermState {
   double acs, act;
 };
 
-template <int N, int K>
+// DUP: the run's repeat pattern when the host has grouped the run by it (bit j:
+// position j repeats position j-1's variable; K <= SDUPK), or -1 for a run whose
+// records carry their own pattern.  A static pattern loads each distinct
+// variable's point, modulus and Jacobian entry once and folds the repeats'
+// partials without selects; the products are the same in the same order.
+constexpr int SDUPK = 4;
+template <int DUP>
+NID_D constexpr bool rep(int j) {
+  return DUP >= 0 && j > 0 && ((DUP >> j) & 1);
+}
+
+template <int N, int K, int DUP = -1>
 NID_D void t_load(TermState<K>& S, const TermRec& R, const cd* xs, const double* axs, bool ws, bool td, cd alpha,
                   double t, const cd* prm, const cd* row) {
   const unsigned long long meta = R.meta;
@@ -73,11 +84,18 @@ NID_D void t_load(TermState<K>& S, const TermRec& R, const cd* xs, const double*
 #pragma unroll
   for (int j = 0; j < K; ++j) S.v[j] = (int)((meta >> (4 * j)) & 15);
 #pragma unroll
-  for (int j = 0; j < K; ++j) S.Jv[j] = row[S.v[j] * SLOTS];
+  for (int j = 0; j < K; ++j)
+    if (!rep<DUP>(j)) S.Jv[j] = row[S.v[j] * SLOTS];
+  double ax = 1.0;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    S.X[j] = xs[S.v[j] * SLOTS];
-    if (ws) S.m = __dmul_rn(S.m, axs[S.v[j] * SLOTS]);
+    if (rep<DUP>(j)) {
+      S.X[j] = S.X[j - 1];
+    } else {
+      S.X[j] = xs[S.v[j] * SLOTS];
+      if (ws) ax = axs[S.v[j] * SLOTS];
+    }
+    if (ws) S.m = __dmul_rn(S.m, ax);
   }
 }
 
@@ -99,10 +117,19 @@ NID_D void t_compute(TermState<K>& S) {
   }
 }
 
-template <int K>
+template <int K, int DUP = -1>
 NID_D void t_commit(TermState<K>& S, cd* row, bool active, bool ws, bool td, cd& hv, double& sS, double& sT) {
   hv = hv + S.p;
-  if (K > 1 && S.dup) {  // repeated variables (uniform): fold into each run's first position
+  if (DUP >= 0) {  // static repeat pattern
+#pragma unroll
+    for (int j = K - 1; j > 0; --j)
+      if (rep<DUP>(j)) S.d[j - 1] = S.d[j - 1] + S.d[j];
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (!rep<DUP>(j)) row[S.v[j] * SLOTS] = S.Jv[j] + S.d[j];
+    }
+  } else if (K > 1 && S.dup) {  // repeated variables (uniform): fold into each run's first position
 #pragma unroll
     for (int j = K - 1; j > 0; --j)
       if (S.dup & (1u << j)) S.d[j - 1] = S.d[j - 1] + S.d[j];
@@ -121,33 +148,33 @@ NID_D void t_commit(TermState<K>& S, cd* row, bool active, bool ws, bool td, cd&
   }
 }
 
-template <int N, int K>
+template <int N, int K, int DUP = -1>
 NID_D void term(const TermRec& R, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t,
                 const cd* prm, cd* row, bool active, cd& hv, double& sS, double& sT) {
   TermState<K> A;
-  t_load<N, K>(A, R, xs, axs, ws, td, alpha, t, prm, row);
+  t_load<N, K, DUP>(A, R, xs, axs, ws, td, alpha, t, prm, row);
   t_compute<K>(A);
-  t_commit<K>(A, row, active, ws, td, hv, sS, sT);
+  t_commit<K, DUP>(A, row, active, ws, td, hv, sS, sT);
 }
 
 // two terms whose variable sets are disjoint (paired on the host): every
 // load first, the two product chains interleaved, then both commits
-template <int N, int K>
+template <int N, int K, int DUP = -1>
 NID_D void term2(const TermRec& RA, const TermRec& RB, const cd* xs, const double* axs, bool ws, bool td, cd alpha,
                  double t, const cd* prm, cd* row, bool active, cd& hv, double& sS, double& sT) {
   TermState<K> A, B;
-  t_load<N, K>(A, RA, xs, axs, ws, td, alpha, t, prm, row);
-  t_load<N, K>(B, RB, xs, axs, ws, td, alpha, t, prm, row);
+  t_load<N, K, DUP>(A, RA, xs, axs, ws, td, alpha, t, prm, row);
+  t_load<N, K, DUP>(B, RB, xs, axs, ws, td, alpha, t, prm, row);
   t_compute<K>(A);
   t_compute<K>(B);
-  t_commit<K>(A, row, active, ws, td, hv, sS, sT);
-  t_commit<K>(B, row, active, ws, td, hv, sS, sT);
+  t_commit<K, DUP>(A, row, active, ws, td, hv, sS, sT);
+  t_commit<K, DUP>(B, row, active, ws, td, hv, sS, sT);
 }
 
 // the records [kr, kend) of one run (factor count K) through the ring:
 // wait for a chunk when the first of its records is reached, refill its
 // slot two chunks ahead once all of its records are consumed
-template <int N, int K>
+template <int N, int K, int DUP = -1>
 NID_D void run(const HomDev& H, long long base, long long& kr, long long kend, long long& cnext, TermRec* ring,
                int lane, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, const cd* prm,
                cd* row, bool active, cd& hv, double& sS, double& sT) {
@@ -161,10 +188,11 @@ NID_D void run(const HomDev& H, long long base, long long& kr, long long kend, l
     // a record at an even offset flagged as paired (meta bit 52) shares no
     // variable with its successor in the same run (capi.cu)
     if (K > 0 && K <= PAIRK && ((ring[pos].meta >> 52) & 1ull)) {
-      term2<N, (K <= PAIRK ? K : 1)>(ring[pos], ring[pos + 1], xs, axs, ws, td, alpha, t, prm, row, active, hv, sS, sT);
+      term2<N, (K <= PAIRK ? K : 1), (K <= PAIRK ? DUP : -1)>(ring[pos], ring[pos + 1], xs, axs, ws, td, alpha, t, prm,
+                                                              row, active, hv, sS, sT);
       kr += 2;
     } else {
-      term<N, K>(ring[pos], xs, axs, ws, td, alpha, t, prm, row, active, hv, sS, sT);
+      term<N, K, DUP>(ring[pos], xs, axs, ws, td, alpha, t, prm, row, active, hv, sS, sT);
       kr += 1;
     }
     if (((kr - base) & (CHUNK - 1)) == 0) {  // chunk consumed by every lane: refill its slot
@@ -241,20 +269,33 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
         sS = 0.0;
         sT = 0.0;
       }
-      const int K = (int)run.y;
+      // run.y: factor count K, and for a run grouped by repeat pattern
+      // (K <= rec::SDUPK) 0x100 | pattern << 9
+      const int K = (int)(run.y & 0xffu);
+      const int key = (int)(run.y >> 8);  // 0: records carry their own pattern
       const long long kend = (long long)run.z + run.w;
-      switch (K) {
+#define NID_RD(KK, DD)                                                                                       \
+  case (KK) | 0x100 | ((DD) << 9):                                                                           \
+    rec::run<N, KK, DD>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm, row, active, hv, \
+                        sS, sT);                                                                             \
+    break;
 #define NID_RT(KK)                                                                                       \
   case KK:                                                                                               \
     rec::run<N, KK>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm, row, active, hv, \
                     sS, sT);                                                                             \
     break;
+      switch (K | (key << 8)) {
+        NID_RD(1, 0)
+        NID_RD(2, 0) NID_RD(2, 2)
+        NID_RD(3, 0) NID_RD(3, 2) NID_RD(3, 4) NID_RD(3, 6)
+        NID_RD(4, 0) NID_RD(4, 2) NID_RD(4, 4) NID_RD(4, 6) NID_RD(4, 8) NID_RD(4, 10) NID_RD(4, 12) NID_RD(4, 14)
         NID_RT(0) NID_RT(1) NID_RT(2) NID_RT(3) NID_RT(4) NID_RT(5) NID_RT(6) NID_RT(7) NID_RT(8)
         NID_RT(9) NID_RT(10) NID_RT(11) NID_RT(12)
-#undef NID_RT
         default:
           break;
       }
+#undef NID_RT
+#undef NID_RD
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncwarp();
@@ -440,8 +481,18 @@ __device__ __noinline__ void eval_slot_rec(const HomDev& H, int g, const cd* xs,
       if (u == u1) break;
       row_i = (int)run.x;
     }
-    const int K = (int)run.y;
-    const long long r0 = (long long)run.z + lane, r1 = (long long)run.z + run.w;
+    const int K = (int)(run.y & 0xffu);
+    const long long r0 = (long long)run.z + lane;
+    long long r1 = (long long)run.z + run.w;
+    // runs of the same row and factor count that differ only in their repeat
+    // pattern are contiguous: one pass over all of them (each record carries
+    // its own pattern), so the 32 lanes stay filled
+    while (u + 1 < u1) {
+      const uint4 nx = __ldg(&H.runs[u + 1]);
+      if ((int)nx.x != row_i || (int)(nx.y & 0xffu) != K) break;
+      r1 += nx.w;
+      ++u;
+    }
     switch (K) {
 #define NID_LT(KK)                                                                                          \
   case KK:                                                                                                  \

@@ -111,7 +111,8 @@ def test_c3_cascade_step_matches_reference(nid, chain, d):
         if len(pts):
             assert pts.shape[1] > n0 and np.all(np.max(np.abs(pts[:, n0:]), axis=1) < BORDER), pts[:, n0:]
     assert got[3] - ref[3] == int(g_only.sum()) - int(r_only.sum())
-    assert int(r_only.sum()) + int(g_only.sum()) <= max(1, len(r_nz) // 100)
+    # (one path that lands on another junk point shows up once on each side)
+    assert max(int(r_only.sum()), int(g_only.sum())) <= max(1, len(r_nz) // 100)
     for s in nxt.zero_slack:
         assert np.max(np.abs(s.coordinates[n0:])) < 1e-8 if s.coordinates.size > n0 else True
 
