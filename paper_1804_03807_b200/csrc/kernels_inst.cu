@@ -21,6 +21,23 @@ static int blocks_for(const void* fn, int threads, int smem = 0) {
   return sms * per;
 }
 
+// Grid of a tracker launch: as many blocks as stay resident (cap), at least one
+// per 32 paths -- and a launch smaller than the machine is dealt round the SMs
+// (one block per path up to the SM count) instead of being packed 32 to a block.
+static int track_grid(long long P, int cap, int max_blocks, int* is_static) {
+  int dev = 0, sms = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long need = (P + rows::SLOTS - 1) / rows::SLOTS;
+  long long spread = P < sms ? P : sms;
+  long long blocks = need > spread ? need : spread;
+  if (blocks > cap) blocks = cap;
+  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
+  if (blocks < 1) blocks = 1;
+  *is_static = blocks * rows::SLOTS >= P ? 1 : 0;
+  return (int)blocks;
+}
+
 #define CAT_(a, b) a##b
 #define CAT(a, b) CAT_(a, b)
 
@@ -30,13 +47,8 @@ int CAT(launch_track_, NID_N)(const TrackArgs& a, int max_blocks, cudaStream_t s
   const int threads = 32 * rows::groups<NID_N>();
   const int smem = (int)ctl::smem_bytes<NID_N>();
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int blocks = blocks_for(fn, threads, smem);
-  long long need = (a.P + rows::SLOTS - 1) / rows::SLOTS;
-  if (need < blocks) blocks = (int)need;
-  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
-  if (blocks < 1) blocks = 1;
   TrackArgs b = a;
-  b.static_claim = need <= blocks ? 1 : 0;
+  const int blocks = track_grid(a.P, blocks_for(fn, threads, smem), max_blocks, &b.static_claim);
   track_ctl_kernel<NID_N><<<blocks, threads, smem, s>>>(b);
   return blocks;
 }
@@ -49,13 +61,8 @@ int CAT(launch_track_pt_, NID_N)(const TrackArgsPT& a, int max_blocks, cudaStrea
   const int threads = 32 * rows::groups<NID_N>();
   const int smem = (int)ctl::Lay<NID_N>::bytes();
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int blocks = blocks_for(fn, threads, smem);
-  long long need = (a.a.P + rows::SLOTS - 1) / rows::SLOTS;
-  if (need < blocks) blocks = (int)need;
-  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
-  if (blocks < 1) blocks = 1;
   TrackArgsPT* b = new TrackArgsPT(a);  // ~22 KB: off the stack
-  b->a.static_claim = need <= blocks ? 1 : 0;
+  const int blocks = track_grid(a.a.P, blocks_for(fn, threads, smem), max_blocks, &b->a.static_claim);
   if (a.t.poly)
     track_pt_kernel<NID_N, true><<<blocks, threads, smem, s>>>(*b);
   else

@@ -32,7 +32,7 @@ struct TrackArgs {
   double* trace;
   int* trace_n;
   int trace_cap;
-  int static_claim;  // P <= blocks x 32: slot s of block b tracks path 32 b + s (set by the launcher)
+  int static_claim;  // P <= blocks x 32: slot s of block b tracks path s * blocks + b (set by the launcher)
 };
 
 // control actions

