@@ -335,6 +335,18 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
       grp[best].push_back(cr.second);
       load[best] += cr.first;
     }
+    if (const char* ov = getenv("NID_ROW_GROUPS")) {  // experiment knob: "g(row 0),g(row 1),..."
+      std::vector<int> gi;
+      for (const char* c = ov; *c;) {
+        gi.push_back(atoi(c));
+        while (*c && *c != ',') ++c;
+        if (*c == ',') ++c;
+      }
+      if ((int)gi.size() == n) {
+        for (int gg = 0; gg < G; ++gg) grp[gg].clear();
+        for (int i = 0; i < n; ++i) grp[(gi[i] % G + G) % G].push_back(i);
+      }
+    }
     int pos = 0;
     for (int gg = 0; gg <= 16; ++gg) h->goff[gg] = 0;
     for (int gg = 0; gg < G; ++gg) {
