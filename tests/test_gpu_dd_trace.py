@@ -134,3 +134,55 @@ def test_double_double_membership_parameters(nid):
     v2, _ = filtering.membership_batch(W, Q, params=TrackParams(precision="double_double"))
     assert np.array_equal(v1, v2)
     assert np.array_equal(v1 == 1, g["verdict"][:8].astype(bool))
+
+
+def test_decompose_in_double_double(nid):
+    """decompose(precision="dd") (blackbox.py:57-60: TrackParams(precision=
+    "double_double") through every stage; the mixed cells of the polyhedral
+    start are tracked in double, see polyhedral._cell_params) on the C3-mini
+    system: the same witness-set degrees as the double-precision run, every
+    start accounted for at every level, and isolated points that are all among
+    the double-precision ones.  Counts are not equal to the double run's: without
+    the evaluation-noise floor (tracker.py:177-181 through `_DDView`) a path
+    whose coordinates grow cannot meet the fixed corrector tolerance and ends
+    FAILED instead of at infinity (test_double_double_diverging_paths pins that
+    to the reference), and a few finite paths are lost with them."""
+    from paper_1804_03807_b200 import blackbox
+    from test_polyhedral import _cells_from
+
+    g = golden("decompose_c3m")
+    pd = configs.c3_mini()
+    cells = _cells_from(g, int(g["n"]), pd.emb.system)
+    a = blackbox.decompose(pd.f, top_dimension=pd.emb.k, seed=pd.seed, cells=cells)
+    b = blackbox.decompose(pd.f, top_dimension=pd.emb.k, seed=pd.seed, cells=cells, precision="dd")
+    assert b.precision == "dd" and a.precision == "double"
+    assert a.degrees == b.degrees == {2: 4}
+    for c in b.cascade_counts:
+        assert c["starts"] == c["at_infinity"] + c["zero_slack"] + c["nonzero_slack"] + c["failures"]
+    assert b.cascade_counts[0]["starts"] == a.cascade_counts[0]["starts"] == 256
+    assert 0.9 * len(a.isolated) <= len(b.isolated) <= len(a.isolated) == 80
+    A = np.array([s.coordinates for s in a.isolated])
+    B = np.array([s.coordinates for s in b.isolated])
+    d = np.abs(A[:, None, :] - B[None, :, :]).max(axis=2)
+    assert d.min(axis=0).max() < 1e-8  # every dd isolated point is a double-precision one
+
+
+def test_double_double_diverging_paths(nid):
+    """16 paths of the C3-mini top continuation tracked by the reference in
+    double and in double-double (tests/golden/make_dd_c3m.py): finite sets equal
+    in both modes, and the paths the reference fails in double-double (for lack
+    of a noise floor) fail here too -- statuses agree on >= 14 of 16."""
+    from paper_1804_03807_b200 import cascade
+
+    g = golden("track_c3m_dd")
+    pd = configs.c3_mini()
+    h, _ = cascade.top_homotopy(pd.emb)
+    for name, prm in (("double", TrackParams()), ("dd", TrackParams(precision="double_double"))):
+        res = tracker.track_batch(h, g["starts"], prm)
+        st = g[f"{name}_status"].astype(int)
+        fin = np.isin(st, (0, 2))
+        assert np.array_equal(res.succeeded, fin), (name, res.status, st)
+        assert int(np.sum(res.status.astype(int) == st)) >= 14, (name, res.status, st)
+        assert np.all(rel_rows(res.x[fin], g[f"{name}_x"][fin]) < 1e-8)
+    # the two modes really differ on this sample
+    assert np.sum(g["dd_status"] == 3) > np.sum(g["double_status"] == 3)
