@@ -32,7 +32,7 @@ NID_D unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shar
 
 // one chunk of records [r0, r0 + 8) into the ring slot `buf` (every lane one
 // 16-byte piece), committed as its own group
-NID_D void fetch(const TermRec* recs, long long r0, TermRec* buf, int lane) {
+NID_D void fetch(const TermRec* recs, int r0, TermRec* buf, int lane) {
   const char* src = reinterpret_cast<const char*>(recs + r0) + lane * 16;
   const unsigned dst = smem_u32(reinterpret_cast<char*>(buf) + lane * 16);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
@@ -175,7 +175,7 @@ NID_D void term2(const TermRec& RA, const TermRec& RB, const cd* xs, const doubl
 // wait for a chunk when the first of its records is reached, refill its
 // slot two chunks ahead once all of its records are consumed
 template <int N, int K, int DUP = -1>
-NID_D void run(const HomDev& H, long long base, long long& kr, long long kend, long long& cnext, TermRec* ring,
+NID_D void run(const HomDev& H, int base, int& kr, int kend, int& cnext, TermRec* ring,
                int lane, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, const cd* prm,
                cd* row, bool active, cd& hv, double& sS, double& sT) {
 #pragma unroll 1
@@ -221,13 +221,14 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
   double r2 = 0.0, mS = 0.0, mT = 0.0;
   const int u0 = H.grun[g], u1 = H.grun[g + 1];
   if (u0 < u1) {
-    const long long base = __ldg(&H.runs[u0]).z;  // the group's first record
-    long long cnext = base;                        // next chunk to fetch
+    // record indices fit 32 bits (a table of 2^31 records would be 128 GB)
+    const int base = (int)__ldg(&H.runs[u0]).z;  // the group's first record
+    int cnext = base;                             // next chunk to fetch
     rec::fetch(H.rec, cnext, ring, lane);
     cnext += rec::CHUNK;
     rec::fetch(H.rec, cnext, ring + rec::CHUNK, lane);
     cnext += rec::CHUNK;
-    long long kr = base;  // the next record to evaluate
+    int kr = base;  // the next record to evaluate
     int row_i = -1;
     cd* row = aug;
     cd hv = cd{0.0, 0.0};
@@ -273,7 +274,7 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
       // (K <= rec::SDUPK) 0x100 | pattern << 9
       const int K = (int)(run.y & 0xffu);
       const int key = (int)(run.y >> 8);  // 0: records carry their own pattern
-      const long long kend = (long long)run.z + run.w;
+      const int kend = (int)(run.z + run.w);
 #define NID_RD(KK, DD)                                                                                       \
   case (KK) | 0x100 | ((DD) << 9):                                                                           \
     rec::run<N, KK, DD>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm, row, active, hv, \
