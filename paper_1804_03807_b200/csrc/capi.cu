@@ -487,7 +487,13 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
             while (q1 < byk.size() && byk[q1].first == byk[q].first) ++q1;
             const int deg_q = byk[q].first >> 12;
             const unsigned ykey = (unsigned)deg_q | ((byk[q].first & 0x800) ? (0x100u | ((unsigned)(byk[q].first & 0x7ff) << 9)) : 0u);
-            runs.push_back(make_uint4((unsigned)i, ykey, (unsigned)recs.size(), (unsigned)(q1 - q)));
+            // bit 30: some term of the run takes a per-path coefficient (membership
+            // targets): only such runs look at the records' parameter slots
+            unsigned hasp = 0u;
+            if (d->param_slot)
+              for (size_t z = q; z < q1; ++z)
+                if (d->param_slot[byk[z].second] >= 0) hasp = 1u << 30;
+            runs.push_back(make_uint4((unsigned)i, ykey | hasp, (unsigned)recs.size(), (unsigned)(q1 - q)));
             // order the run so records at even offsets from the group's first
             // record pair with a successor of disjoint variables (greedy, first
             // fit within a window): the evaluator interleaves such pairs

@@ -273,16 +273,17 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
       // run.y: factor count K, and for a run grouped by repeat pattern
       // (K <= rec::SDUPK) 0x100 | pattern << 9
       const int K = (int)(run.y & 0xffu);
-      const int key = (int)(run.y >> 8);  // 0: records carry their own pattern
+      const int key = (int)((run.y >> 8) & 0x3fffu);  // 0: records carry their own pattern
+      const cd* const prm_run = ((run.y >> 30) & 1u) ? prm : nullptr;  // runs without parameter slots skip the test
       const int kend = (int)(run.z + run.w);
 #define NID_RD(KK, DD)                                                                                       \
   case (KK) | 0x100 | ((DD) << 9):                                                                           \
-    rec::run<N, KK, DD>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm, row, active, hv, \
+    rec::run<N, KK, DD>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm_run, row, active, hv, \
                         sS, sT);                                                                             \
     break;
 #define NID_RT(KK)                                                                                       \
   case KK:                                                                                               \
-    rec::run<N, KK>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm, row, active, hv, \
+    rec::run<N, KK>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm_run, row, active, hv, \
                     sS, sT);                                                                             \
     break;
       switch (K | (key << 8)) {
