@@ -494,9 +494,11 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
               for (size_t z = q; z < q1; ++z)
                 if (d->param_slot[byk[z].second] >= 0) hasp = 1u << 30;
             runs.push_back(make_uint4((unsigned)i, ykey | hasp, (unsigned)recs.size(), (unsigned)(q1 - q)));
-            // order the run so records at even offsets from the group's first
-            // record pair with a successor of disjoint variables (greedy, first
-            // fit within a window): the evaluator interleaves such pairs
+            // Order the run as [one single if the run starts at an odd offset from the
+            // group's first record] [pairs of terms with disjoint variables (greedy, first
+            // fit within a window): the evaluator interleaves their product chains] [the
+            // remaining singles]; the run descriptor carries the lead flag (y bit 28) and
+            // the pair count (y bits 16..27), so the evaluator tells a pair by position.
             std::vector<int> pend;
             for (size_t z = q; z < q1; ++z) pend.push_back(byk[z].second);
             auto vmask = [&](int k) {
@@ -505,29 +507,43 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
                 if (d->expo[k * NID_MAX_VARS + v]) mk |= 1u << v;
               return mk;
             };
-            std::vector<std::pair<int, bool>> order;  // (term, paired with the next)
-            size_t gpos = recs.size() - (size_t)grp_base;
+            std::vector<std::pair<int, int>> pairs;
+            std::vector<int> singles;
             while (!pend.empty()) {
               const int a = pend.front();
               pend.erase(pend.begin());
               bool paired = false;
-              if ((gpos & 1) == 0 && deg_q > 0 && deg_q <= 6) {  // rec::PAIRK
+              if (deg_q > 0 && deg_q <= 6 && pairs.size() < 4095) {  // rec::PAIRK
                 const unsigned ma = vmask(a);
                 for (size_t z = 0; z < pend.size() && z < 64; ++z)
                   if (!(vmask(pend[z]) & ma)) {
-                    order.push_back({a, true});
-                    order.push_back({pend[z], false});
+                    pairs.push_back({a, pend[z]});
                     pend.erase(pend.begin() + z);
                     paired = true;
-                    gpos += 2;
                     break;
                   }
               }
-              if (!paired) {
-                order.push_back({a, false});
-                gpos += 1;
-              }
+              if (!paired) singles.push_back(a);
             }
+            const bool odd = ((recs.size() - (size_t)grp_base) & 1) != 0;
+            if (odd && !pairs.empty() && singles.empty()) {  // no single to realign with: split a pair
+              singles.push_back(pairs.back().first);
+              singles.push_back(pairs.back().second);
+              pairs.pop_back();
+            }
+            std::vector<std::pair<int, bool>> order;  // (term, paired with the next)
+            unsigned lead = 0u;
+            if (odd && !pairs.empty()) {
+              order.push_back({singles.front(), false});
+              singles.erase(singles.begin());
+              lead = 1u;
+            }
+            for (auto& pr : pairs) {
+              order.push_back({pr.first, true});
+              order.push_back({pr.second, false});
+            }
+            for (int k1 : singles) order.push_back({k1, false});
+            runs.back().y |= (lead << 28) | ((unsigned)pairs.size() << 16);
             for (size_t z = 0; z < order.size(); ++z) {
               const int k = order[z].first;
               TermRec r;

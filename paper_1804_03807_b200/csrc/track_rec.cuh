@@ -175,7 +175,7 @@ NID_D void term2(const TermRec& RA, const TermRec& RB, const cd* xs, const doubl
 // wait for a chunk when the first of its records is reached, refill its
 // slot two chunks ahead once all of its records are consumed
 template <int N, int K, int DUP = -1>
-NID_D void run(const HomDev& H, int base, int& kr, int kend, int& cnext, TermRec* ring,
+NID_D void run(const HomDev& H, int base, int& kr, int kend, int p0, int p1, int& cnext, TermRec* ring,
                int lane, const cd* xs, const double* axs, bool ws, bool td, cd alpha, double t, const cd* prm,
                cd* row, bool active, cd& hv, double& sS, double& sT) {
 #pragma unroll 1
@@ -185,9 +185,9 @@ NID_D void run(const HomDev& H, int base, int& kr, int kend, int& cnext, TermRec
       wait_one();
       __syncwarp();
     }
-    // a record at an even offset flagged as paired (meta bit 52) shares no
-    // variable with its successor in the same run (capi.cu)
-    if (K > 0 && K <= PAIRK && ((ring[pos].meta >> 52) & 1ull)) {
+    // records [p0, p1) of the run are pairs at even offsets whose two terms share
+    // no variable (capi.cu lays a run out as lead single, pairs, singles)
+    if (K > 0 && K <= PAIRK && kr >= p0 && kr < p1) {
       term2<N, (K <= PAIRK ? K : 1), (K <= PAIRK ? DUP : -1)>(ring[pos], ring[pos + 1], xs, axs, ws, td, alpha, t, prm,
                                                               row, active, hv, sS, sT);
       kr += 2;
@@ -273,17 +273,19 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
       // run.y: factor count K, and for a run grouped by repeat pattern
       // (K <= rec::SDUPK) 0x100 | pattern << 9
       const int K = (int)(run.y & 0xffu);
-      const int key = (int)((run.y >> 8) & 0x3fffu);  // 0: records carry their own pattern
+      const int key = (int)((run.y >> 8) & 0xffu);  // 0: records carry their own pattern
       const cd* const prm_run = ((run.y >> 30) & 1u) ? prm : nullptr;  // runs without parameter slots skip the test
       const int kend = (int)(run.z + run.w);
+      const int p0 = (int)run.z + (int)((run.y >> 28) & 1u);          // first pair
+      const int p1 = p0 + 2 * (int)((run.y >> 16) & 0xfffu);          // one past the last pair
 #define NID_RD(KK, DD)                                                                                       \
   case (KK) | 0x100 | ((DD) << 9):                                                                           \
-    rec::run<N, KK, DD>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm_run, row, active, hv, \
+    rec::run<N, KK, DD>(H, base, kr, kend, p0, p1, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm_run, row, active, hv, \
                         sS, sT);                                                                             \
     break;
 #define NID_RT(KK)                                                                                       \
   case KK:                                                                                               \
-    rec::run<N, KK>(H, base, kr, kend, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm_run, row, active, hv, \
+    rec::run<N, KK>(H, base, kr, kend, p0, p1, cnext, ring, lane, xs, axw, ws, td, alpha, t, prm_run, row, active, hv, \
                     sS, sT);                                                                             \
     break;
       switch (K | (key << 8)) {
