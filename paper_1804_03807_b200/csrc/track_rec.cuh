@@ -17,6 +17,15 @@
 // leave-one-out products of its positions sum to a * x^(a-1) * rest.  A
 // position that repeats the previous variable folds its partial into the
 // first position of the run, which alone updates the Jacobian entry.
+//
+// Runs (capi.cu): a row's terms are grouped by factor count and, up to four
+// factors, by repeat pattern (run descriptor y: count | 0x100 | pattern << 9),
+// so those runs' term bodies are instantiated per pattern: repeats fold
+// statically and each distinct variable is loaded once.  Inside a run the
+// records are laid out as [lead single][pairs of terms with disjoint
+// variables][singles] (y bit 28, bits 16..27): a pair is told by its position
+// and its two product chains are interleaved.  y bit 30 marks runs with
+// per-path coefficients (membership targets); other runs skip that test.
 #pragma once
 #include "track_rows.cuh"
 
