@@ -61,6 +61,7 @@ struct NidHomotopy {
   PTab* ptab = nullptr;  // host copy of the parameter-bank table (null: table too large / per-path params)
   TermRec* rec = nullptr;  // streamed records (csrc/track_rec.cuh), n > 10
   uint4* runs = nullptr;
+  std::vector<uint4> hruns;  // host copy: travels with every launch (TrackArgs::runs_c)
   int grun[17] = {0};
   HomDev dev() const {
     HomDev h;
@@ -582,7 +583,8 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
       if (!e) e = cudaMemcpy(h->rec, recs.data(), recs.size() * sizeof(TermRec), cudaMemcpyHostToDevice);
       if (!e) e = cudaMalloc(&h->runs, (runs.size() + 1) * sizeof(uint4));
       if (!e && !runs.empty()) e = cudaMemcpy(h->runs, runs.data(), runs.size() * sizeof(uint4), cudaMemcpyHostToDevice);
-      if (e || getenv("NID_NO_REC")) {
+      h->hruns = runs;
+      if (e || getenv("NID_NO_REC") || runs.size() > (size_t)NID_MAX_RUNS) {
         cudaFree(h->rec);
         cudaFree(h->runs);
         h->rec = nullptr;
@@ -807,6 +809,7 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   // per-slot evaluation (streamed-record tracker, n >= 8) when a block has at
   // most lat_slots evaluating slots: the drain of a launch and launches smaller
   // than the machine, where a level lasts as long as its slowest paths
+  for (size_t u = 0; u < h->hruns.size() && u < (size_t)NID_MAX_RUNS; ++u) a.runs_c[u] = h->hruns[u];
   a.lat_slots = 8;
   if (getenv("NID_LAT_SLOTS")) a.lat_slots = atoi(getenv("NID_LAT_SLOTS"));
   if (!a.gstate) FAIL("out of device memory (slot state)");

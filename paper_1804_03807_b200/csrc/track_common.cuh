@@ -4,6 +4,8 @@
 #include "homotopy.cuh"
 #include "linalg.cuh"
 
+constexpr int NID_MAX_RUNS = 256;
+
 struct TrackArgs {
   HomDev H;
   NidTrackParams prm;
@@ -33,6 +35,10 @@ struct TrackArgs {
   int* trace_n;
   int trace_cap;
   int static_claim;  // P <= blocks x 32: slot s of block b tracks path s * blocks + b (set by the launcher)
+  // the streamed-record evaluator's run descriptors (HomDev::runs) in the launch's
+  // parameter bank: loop bounds, factor counts and patterns are then uniform
+  // constant-bank loads (a table with more runs is not streamed)
+  uint4 runs_c[NID_MAX_RUNS];
 };
 
 // control actions

@@ -782,7 +782,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
         const cd* prm = (act && pr >= 0) ? Ar.params + pr : nullptr;
         TermRec* ring = reinterpret_cast<TermRec*>(smem_ctl + L::bytes()) + g * 2 * rec::CHUNK;
         if (__any_sync(0xffffffffu, act))
-          eval_rows_rec<N>(Ar.H, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+          eval_rows_rec<N>(Ar.H, Ar.runs_c, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
                            db + L::AXW * S + lane, ring);
         // few evaluating slots: one slot at a time, the warp's lanes split the terms
         unsigned lm = __ballot_sync(0xffffffffu, lat);

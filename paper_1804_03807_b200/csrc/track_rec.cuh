@@ -219,8 +219,8 @@ NID_D void run(const HomDev& H, int base, int& kr, int kend, int p0, int p1, int
 // 32 lanes); `active` lanes own an evaluating slot and alone write it.
 // ring: this warp's 2 x 8 records of shared memory.
 template <int N>
-NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const cd* prm, cd* aug, double* dbl,
-                         bool want_scale, bool active, double* axw, TermRec* ring) {
+NID_D void eval_rows_rec(const HomDev& H, const uint4* runs, int g, const cd* xs, double t, const cd* prm, cd* aug,
+                         double* dbl, bool want_scale, bool active, double* axw, TermRec* ring) {
   using L = rows::Layout<N>;
   constexpr int S = rows::SLOTS;
   const int lane = threadIdx.x & 31;
@@ -228,10 +228,12 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
   const bool ws = __any_sync(0xffffffffu, want_scale && active);
   const bool td = H.td != 0;
   double r2 = 0.0, mS = 0.0, mT = 0.0;
-  const int u0 = H.grun[g], u1 = H.grun[g + 1];
+  // the warp's group index through a shuffle: the compiler then knows it is uniform
+  const int gu = __shfl_sync(0xffffffffu, g, 0);
+  const int u0 = H.grun[gu], u1 = H.grun[gu + 1];
   if (u0 < u1) {
     // record indices fit 32 bits (a table of 2^31 records would be 128 GB)
-    const int base = (int)__ldg(&H.runs[u0]).z;  // the group's first record
+    const int base = (int)runs[u0].z;  // the group's first record
     int cnext = base;                             // next chunk to fetch
     rec::fetch(H.rec, cnext, ring, lane);
     cnext += rec::CHUNK;
@@ -244,7 +246,7 @@ NID_D void eval_rows_rec(const HomDev& H, int g, const cd* xs, double t, const c
     double sS = 0.0, sT = 0.0;
 #pragma unroll 1
     for (int u = u0; u <= u1; ++u) {
-      const uint4 run = u < u1 ? __ldg(&H.runs[u]) : make_uint4(0xffffffffu, 0u, 0u, 0u);
+      const uint4 run = u < u1 ? runs[u] : make_uint4(0xffffffffu, 0u, 0u, 0u);
       if ((int)run.x != row_i) {
         if (row_i >= 0) {  // close the previous row: start system, -H, partial maxima
           if (td) {  // G_i = x_i^{d_i} - 1 in closed form
