@@ -25,6 +25,18 @@ def test_c5_full_scale_properties(nid):
     fin = res.succeeded
     nf = int(fin.sum())
     assert 0.6 * C5_MIXED_VOLUME < nf <= C5_MIXED_VOLUME
+    # the reference's own uniform sample of these paths (131,072 indices tracked by
+    # nidpipe, tests/golden/make_fullsize.py) puts the full count at
+    # finite_sample / sample * paths with a binomial standard deviation of
+    # sqrt(finite_sample) / sample * paths: the full run must lie within 3 sigma, and
+    # on the sampled indices themselves it must have exactly the reference's finite set
+    from conftest import golden
+
+    fix = golden("track_c5_full_sample")
+    ns, fs = len(fix["index"]), int(np.isin(fix["status"], (0, 2)).sum())
+    expect, sigma = fs / ns * p.paths, np.sqrt(fs) / ns * p.paths
+    assert abs(nf - expect) < 3 * sigma, (nf, expect, sigma)
+    assert np.array_equal(fin[fix["index"]], np.isin(fix["status"], (0, 2)))
     assert np.all(res.residual[fin] <= 1e-8)
     X = res.x[fin]
     Hv, _, _ = LinearHomotopy(p.target, p.target).evaluate(X, np.ones(len(X)))
