@@ -63,6 +63,10 @@ struct NidHomotopy {
   uint4* runs = nullptr;
   std::vector<uint4> hruns;  // host copy: travels with every launch (TrackArgs::runs_c)
   int grun[17] = {0};
+  uint4* crec = nullptr;      // column-owner stream (csrc/track_col.cuh) or null
+  std::vector<uint4> hcruns;  // its run descriptors: travel with the launch instead of hruns
+  int cgrun[17] = {0};
+  int cgbase[17] = {0};
   HomDev dev() const {
     HomDev h;
     h.n = n;
@@ -88,10 +92,15 @@ struct NidHomotopy {
     h.rec = rec;
     h.runs = runs;
     for (int v = 0; v <= 16; ++v) h.grun[v] = grun[v];
+    h.crec = crec;
+    for (int v = 0; v <= 16; ++v) h.cgrun[v] = cgrun[v];
+    for (int v = 0; v <= 16; ++v) h.cgbase[v] = cgbase[v];
     h.dd = 0;
     return h;
   }
 };
+
+#include "col_lower.h"
 
 // grow-only device workspace slots
 struct Buf {
@@ -590,6 +599,17 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
         h->rec = nullptr;
         h->runs = nullptr;
       }
+      // the column-owner stream (csrc/track_col.cuh) beside the records, which
+      // stay for the per-slot evaluator; n = 8 .. 14 (ctl::lat_on<n>(): the
+      // partial sums of the values use the per-slot scratch)
+      if (!e && h->rec && n <= 14 && !getenv("NID_NO_COL")) {
+        std::vector<uint4> pieces, cruns;
+        if (colhost::build(d, n, T, off, acs, act, G, h->td != 0, pieces, cruns, h->cgrun, h->cgbase)) {
+          e = cudaMalloc(&h->crec, pieces.size() * sizeof(uint4));
+          if (!e) e = cudaMemcpy(h->crec, pieces.data(), pieces.size() * sizeof(uint4), cudaMemcpyHostToDevice);
+          h->hcruns = cruns;
+        }
+      }
     }
   }
   if (!e && T) e = cudaMemcpy(h->cs, d->coef_start, T * sizeof(cd), cudaMemcpyHostToDevice);
@@ -616,6 +636,7 @@ int nid_homotopy_destroy(NidHomotopy* h) {
   cudaFree(h->fex);
   if (h->rec) cudaFree(h->rec);
   if (h->runs) cudaFree(h->runs);
+  if (h->crec) cudaFree(h->crec);
   cudaFree(h->cs);
   cudaFree(h->ct);
   cudaFree(h->acs);
@@ -809,7 +830,9 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   // per-slot evaluation (streamed-record tracker, n >= 8) when a block has at
   // most lat_slots evaluating slots: the drain of a launch and launches smaller
   // than the machine, where a level lasts as long as its slowest paths
-  for (size_t u = 0; u < h->hruns.size() && u < (size_t)NID_MAX_RUNS; ++u) a.runs_c[u] = h->hruns[u];
+  // (the column-owner stream's descriptors when the table has one: track_col.cuh)
+  const std::vector<uint4>& lruns = h->crec ? h->hcruns : h->hruns;
+  for (size_t u = 0; u < lruns.size() && u < (size_t)NID_MAX_RUNS; ++u) a.runs_c[u] = lruns[u];
   a.lat_slots = 8;
   if (getenv("NID_LAT_SLOTS")) a.lat_slots = atoi(getenv("NID_LAT_SLOTS"));
   if (!a.gstate) FAIL("out of device memory (slot state)");

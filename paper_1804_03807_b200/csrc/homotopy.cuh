@@ -62,6 +62,12 @@ struct HomDev {
   const TermRec* rec;
   const uint4* runs;
   int grun[17];
+  // column-owner stream (track_col.cuh) or null: group g walks the runs
+  // [cgrun[g], cgrun[g+1]) of the launch's run descriptors over the pieces
+  // that start at crec + cgbase[g]
+  const uint4* crec;
+  int cgrun[17];
+  int cgbase[17];
   int dd;  // evaluate in complex double-double (auxiliary kernel, track_aux.cuh); set per launch
 };
 

@@ -29,6 +29,7 @@
 #pragma once
 #include "track_ptab.cuh"
 #include "track_rec.cuh"
+#include "track_col.cuh"
 #include "track_rows.cuh"
 
 namespace ctl {
@@ -211,7 +212,9 @@ constexpr bool rec_on() {
 // the parameter-bank kernel needs the slot layout only
 template <int N>
 constexpr size_t ring_bytes() {
-  return rec_on<N>() ? (size_t)rows::groups<N>() * 2 * rec::CHUNK * sizeof(TermRec) : 0;
+  // (the row-per-warp ring needs 2 x 8 records of 64 bytes, the column-owner
+  // ring of track_col.cuh four chunks of 32 pieces: the larger of the two)
+  return rec_on<N>() ? (size_t)rows::groups<N>() * (size_t)col::RP * sizeof(uint4) : 0;
 }
 // per-slot evaluation of long paths, where its scratch fits beside the slot
 // layout and the rings (n = 8 .. 14; not n = 15, 16)
@@ -706,6 +709,27 @@ struct has_table_flag<E, decltype((void)E::kTable)> {
 // table in global memory, read through L1) and the parameter-table kernel
 // (track_pt_kernel: csrc/track_ptab.cuh, the table in the launch's constant
 // bank).  Tab = void selects Eval; Tab = PTab selects PTEval.
+// The streamed-table kernel (n >= 8) re-derives its shared-memory views from an
+// opaque offset at the top of every block-loop iteration: otherwise the
+// compiler hoists the phases' address arithmetic out of the loop and the
+// evaluation phase runs with most of the 255 registers already live (its
+// accumulators were spilled).
+#define NID_LOOP_VIEWS()                                                                                   \
+  unsigned sb_ = 0;                                                                                        \
+  if constexpr (rec_on<N>() && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value)                   \
+    asm volatile("mov.u32 %0, 0;" : "=r"(sb_));                                                            \
+  unsigned char* const smv_ = smem_ctl + sb_;                                                              \
+  cd* const cb = reinterpret_cast<cd*>(smv_);                                                              \
+  double* const db = reinterpret_cast<double*>(cb + (size_t)L::CPLX * S);                                  \
+  long long* const lb = reinterpret_cast<long long*>(db + (size_t)L::DBL * S);                             \
+  int* const ib = reinterpret_cast<int*>(lb + (size_t)L::LLN * S);                                         \
+  cd* const aug = cb + lane;                                                                               \
+  double* const part = db + L::PART * S + lane;                                                            \
+  cd* const augc = cb + cs;                                                                                \
+  double* const partc = db + L::PART * S + cs;                                                             \
+  const SlotView V{cb + L::XE * S + cs, gs + L::GXO * S, gs + L::GXS * S, gs + L::GDS * S, db + cs,        \
+                   ib + cs, lb + cs, cs}
+
 template <int N, class Eval, class Tab, bool PO = false, bool TR = false>
 __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) {
   using namespace ctl;
@@ -748,6 +772,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
 
   while (true) {
     NID_T0();
+    NID_LOOP_VIEWS();
     if (is_ctl) control<N, TR>(Ar, V, augc + N * S);
     __syncwarp();
     {
@@ -766,6 +791,7 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     if (!__syncthreads_or(W_IS(I_ACT) != A_IDLE)) break;
     NID_TP(1);  // barrier before the evaluation
     bool rec_done = false;
+    bool col_done = false;  // block-uniform: this round's block pass was the column-owner one
     if constexpr (rec_on<N>() && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value) {
       if (Ar.H.rec) {  // streamed records: every lane of the warp takes part
         const bool act0 = W_IS(I_ACT) == A_EVAL;
@@ -780,13 +806,24 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
         const bool want = act && (W_IS(I_FLAGS) & (F_NEEDSCALE | F_FALLBACK)) != 0;
         const long long pr = lb[S + lane];
         const cd* prm = (act && pr >= 0) ? Ar.params + pr : nullptr;
-        TermRec* ring = reinterpret_cast<TermRec*>(smem_ctl + L::bytes()) + g * 2 * rec::CHUNK;
-        if (__any_sync(0xffffffffu, act))
-          eval_rows_rec<N>(Ar.H, Ar.runs_c, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
-                           db + L::AXW * S + lane, ring);
+        unsigned char* const ringb = smem_ctl + L::bytes() + (size_t)g * col::RP * sizeof(uint4);
+        unsigned char* scr = smem_ctl + L::bytes() + ring_bytes<N>() + (size_t)g * lat::warp_bytes<N>();
+        if (__any_sync(0xffffffffu, act)) {
+          if (lat_on<N>() && Ar.H.crec) {
+            // column-owner pass (track_col.cuh): the values are left as per-warp
+            // partial sums in this warp's scratch, completed after the barrier
+            eval_cols<N>(Ar.H, Ar.runs_c, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+                         db + L::AXW * S + lane, reinterpret_cast<uint4*>(ringb), reinterpret_cast<cd*>(scr) + lane);
+            col_done = true;
+          } else {
+#ifndef NID_COL_ONLY
+            eval_rows_rec<N>(Ar.H, Ar.runs_c, g, cb + L::XE * S + lane, W_DS(D_TE), prm, aug, part, want, act,
+                             db + L::AXW * S + lane, reinterpret_cast<TermRec*>(ringb));
+#endif
+          }
+        }
         // few evaluating slots: one slot at a time, the warp's lanes split the terms
         unsigned lm = __ballot_sync(0xffffffffu, lat);
-        unsigned char* scr = smem_ctl + L::bytes() + ring_bytes<N>() + (size_t)g * lat::warp_bytes<N>();
 #pragma unroll 1
         while (lat_on<N>() && lm) {
           const int s = __ffs(lm) - 1;
@@ -828,6 +865,14 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
     NID_TP(2);  // evaluation
     __syncthreads();
     NID_TP(3);  // barrier after the evaluation
+    if constexpr (lat_on<N>() && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value) {
+      if (col_done) {
+        const int ss = g * CPW + lane % CPW;
+        col_reduce<N, G, CPW>(Ar.H, g, lane, ib[I_ACT * S + ss] == A_EVAL, cb, db + L::PART * S, cb + L::XE * S,
+                              db[D_TE * S + ss], smem_ctl + L::bytes() + ring_bytes<N>(), lat::warp_bytes<N>());
+        __syncwarp();
+      }
+    }
     if (is_ctl && C_IS(I_ACT) == A_EVAL) {
       double sc = 0.0;
       const double r = rows::combine_resid<N>(augc, partc, C_DS(D_TE), sc, PO);
