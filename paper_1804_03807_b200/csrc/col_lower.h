@@ -86,7 +86,11 @@ inline bool build(const NidHomotopyDesc* d, int n, int T, const std::vector<int>
     return (int)col::C_TWO;
   };
   // records of monomials [m0, m1) for (col, row block) grouped into runs
+  // experiment knob: NID_COL_W="abs weight,values weight" scales the cost model
+  double w_abs = 1.0, w_val = 1.0;
+  if (const char* wv = getenv("NID_COL_W")) sscanf(wv, "%lf,%lf", &w_abs, &w_val);
   auto make_unit = [&](int colv, int row0, int nr, int kind, int m0, int m1) {
+    const double wscale = kind == col::K_ABS ? w_abs : (colv == n ? w_val : 1.0);
     Unit u;
     u.col = colv;
     u.row0 = row0;
@@ -120,9 +124,9 @@ inline bool build(const NidHomotopyDesc* d, int n, int T, const std::vector<int>
       r.recs = kv.second;
       const int pc = popc(r.mask);
       // instructions per record (SASS counts of the run bodies)
-      const double per = kind == col::K_ABS ? 10.0 + 5.0 * r.D + 5.0 * pc
+      const double per = kind == col::K_ABS ? 16.0 + 6.0 * r.D + 5.0 * pc
                                             : 12.0 + 9.0 * r.D + pc * (r.cls >= col::C_TWO ? 11.0 : 5.0);
-      u.cost += 10.0 + per * (double)r.recs.size();
+      u.cost += 10.0 + per * wscale * (double)r.recs.size();
       u.runs.push_back(r);
     }
     u.cost += 20.0;

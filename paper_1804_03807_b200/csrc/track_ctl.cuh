@@ -223,6 +223,11 @@ constexpr bool lat_on() {
   return rec_on<N>() && Lay<N>::bytes() + ring_bytes<N>() + (size_t)rows::groups<N>() * lat::warp_bytes<N>() +
                             1024 <= (size_t)227 * 1024;
 }
+// the host builds the column-owner stream for n = 8 .. 14 (capi.cu) and then
+// passes its run descriptors with the launch: the kernel must take that path
+static_assert(lat_on<8>() && lat_on<9>() && lat_on<10>() && lat_on<11>() && lat_on<12>() && lat_on<13>() &&
+                  lat_on<14>(),
+              "column-owner evaluator needs the per-slot scratch for n = 8 .. 14");
 template <int N>
 constexpr size_t lat_bytes() {
   return lat_on<N>() ? (size_t)rows::groups<N>() * lat::warp_bytes<N>() : 0;
@@ -709,27 +714,6 @@ struct has_table_flag<E, decltype((void)E::kTable)> {
 // table in global memory, read through L1) and the parameter-table kernel
 // (track_pt_kernel: csrc/track_ptab.cuh, the table in the launch's constant
 // bank).  Tab = void selects Eval; Tab = PTab selects PTEval.
-// The streamed-table kernel (n >= 8) re-derives its shared-memory views from an
-// opaque offset at the top of every block-loop iteration: otherwise the
-// compiler hoists the phases' address arithmetic out of the loop and the
-// evaluation phase runs with most of the 255 registers already live (its
-// accumulators were spilled).
-#define NID_LOOP_VIEWS()                                                                                   \
-  unsigned sb_ = 0;                                                                                        \
-  if constexpr (rec_on<N>() && !ctl::is_ptab<Tab>::value && has_table_flag<Eval>::value)                   \
-    asm volatile("mov.u32 %0, 0;" : "=r"(sb_));                                                            \
-  unsigned char* const smv_ = smem_ctl + sb_;                                                              \
-  cd* const cb = reinterpret_cast<cd*>(smv_);                                                              \
-  double* const db = reinterpret_cast<double*>(cb + (size_t)L::CPLX * S);                                  \
-  long long* const lb = reinterpret_cast<long long*>(db + (size_t)L::DBL * S);                             \
-  int* const ib = reinterpret_cast<int*>(lb + (size_t)L::LLN * S);                                         \
-  cd* const aug = cb + lane;                                                                               \
-  double* const part = db + L::PART * S + lane;                                                            \
-  cd* const augc = cb + cs;                                                                                \
-  double* const partc = db + L::PART * S + cs;                                                             \
-  const SlotView V{cb + L::XE * S + cs, gs + L::GXO * S, gs + L::GXS * S, gs + L::GDS * S, db + cs,        \
-                   ib + cs, lb + cs, cs}
-
 template <int N, class Eval, class Tab, bool PO = false, bool TR = false>
 __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) {
   using namespace ctl;
@@ -772,7 +756,6 @@ __device__ __forceinline__ void track_body(const TrackArgs& Ar, const Tab* tab) 
 
   while (true) {
     NID_T0();
-    NID_LOOP_VIEWS();
     if (is_ctl) control<N, TR>(Ar, V, augc + N * S);
     __syncwarp();
     {

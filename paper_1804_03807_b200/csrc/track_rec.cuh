@@ -352,7 +352,10 @@ constexpr size_t warp_bytes() {  // xb[N] cd, 32 lane rows of NP cd, axb[N] doub
 template <int N, int K>
 NID_D void lane_terms(const TermRec* recs, long long r, long long r1, const cd* xb, const double* axb, bool ws,
                       bool td, cd alpha, double t, const cd* prm, cd* jl, cd& hv, double& sS, double& sT) {
+  // (defined on every path: a record first written under `r < r1` counts as live
+  // from the function's entry in each of the 13 instantiations, and is spilled)
   TermRec Rn;
+  memset(&Rn, 0, sizeof(Rn));
   if (r < r1) Rn = recs[r];
 #pragma unroll 1
   for (; r < r1; r += 32) {
