@@ -191,32 +191,97 @@ NID_D bool dd_polish(const Grp<N>& g, const HomDev& H, const cd* prm, const cd (
   return fin;
 }
 
-// SVD of the group's square Jacobian rows (lane lg holds row lg): writes
-// rows to the complex scratch `cs` (N*N + N*N), lane 0 computes the singular
-// values; returns cond and rank to every lane of the group.
+// condition_and_rank (linalg.py:13-32) of the group's Jacobian, one row per
+// lane, by a one-sided (Hestenes) Jacobi SVD run by the whole group: the rows
+// are orthogonalised pairwise (the singular values of J are those of its
+// transpose), N/2 disjoint pairs per round in round-robin order, each lane
+// fetching its partner's row by shuffles and both lanes of a pair forming the
+// same rotation from the same operands; the singular values are the row norms.
+// (The parity hook svd_kernel keeps the serial jacobi_svd of linalg.cuh, which
+// until round 2 also served here on the group's lane 0 over a global scratch
+// slab: 1.2 s of endpoint_kernel<14> for C4's 400,000 endpoints.)  `cs` is unused.
 template <int N>
 NID_D void group_cond_rank(const Grp<N>& g, const cd (&Jrow)[N], cd* cs, double& cond, int& rank) {
+  (void)cs;
+  cd u[N];
+  bool fin = true;
 #pragma unroll
-  for (int v = 0; v < N; ++v) cs[g.lg * N + v] = Jrow[v];
-  __syncwarp(g.mask);
-  double c = 0.0;
-  int r = 0;
-  if (g.lg == 0) {
-    bool fin = true;
-    for (int i = 0; i < N * N; ++i) fin = fin && cfinite(cs[i]);
-    if (!fin) {
-      c = INFINITY;
-      r = 0;
-    } else {
-      double sv[N];
-      jacobi_svd(cs, N, N, N, nullptr, N, sv);
-      sort_desc(sv, N);
-      cond_rank_from_sv(sv, N, SINGULARITY_TOL, c, r);
+  for (int v = 0; v < N; ++v) {
+    u[v] = Jrow[v];
+    fin = fin && cfinite(u[v]);
+  }
+  if (!group_all<N>(g, fin)) {
+    cond = INFINITY;
+    rank = 0;
+    return;
+  }
+  constexpr int M = (N + 1) & ~1;  // players of the round-robin (a dummy for odd N)
+  const double eps = 2.220446049250313e-16;
+  if (N > 1) {
+#pragma unroll 1
+    for (int sweep = 0; sweep < 60; ++sweep) {
+      bool rotated = false;
+#pragma unroll 1
+      for (int r = 0; r < M - 1; ++r) {
+        // circle method: player M-1 stays, the others rotate
+        int partner;
+        if (g.lg == M - 1) {
+          partner = (r * (M / 2)) % (M - 1);
+        } else {
+          partner = (r - g.lg) % (M - 1);
+          if (partner < 0) partner += M - 1;
+          if (partner == g.lg) partner = M - 1;
+        }
+        const bool idle = partner >= N;
+        const int src = g.gbase + (idle ? g.lg : partner);
+        cd w[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[i] = shfl_c(g.mask, u[i], src);
+        if (!idle) {
+          const bool low = g.lg < partner;  // the pair's first vector is the lower lane's row
+          double al = 0.0, be = 0.0;
+          cd ga = cd{0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            const cd ap = low ? u[i] : w[i], aq = low ? w[i] : u[i];
+            al += ap.re * ap.re + ap.im * ap.im;
+            be += aq.re * aq.re + aq.im * aq.im;
+            ga.re += ap.re * aq.re + ap.im * aq.im;  // conj(ap) * aq
+            ga.im += ap.re * aq.im - ap.im * aq.re;
+          }
+          const double gabs = hypot(ga.re, ga.im);
+          if (gabs > eps * sqrt(al * be) && gabs != 0.0) {
+            rotated = true;
+            const cd ph = cd{ga.re / gabs, -ga.im / gabs};  // e^{-i phi}
+            const double zeta = (be - al) / (2.0 * gabs);
+            const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              const cd ap = low ? u[i] : w[i];
+              const cd aq = (low ? w[i] : u[i]) * ph;
+              u[i] = low ? cd{c * ap.re - sn * aq.re, c * ap.im - sn * aq.im}
+                         : cd{sn * ap.re + c * aq.re, sn * ap.im + c * aq.im};
+            }
+          }
+        }
+      }
+      if (!(__ballot_sync(g.mask, rotated) & g.bits)) break;
     }
   }
-  cond = __shfl_sync(g.mask, c, g.gbase);
-  rank = __shfl_sync(g.mask, r, g.gbase);
-  __syncwarp(g.mask);
+  double s2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) s2 += u[i].re * u[i].re + u[i].im * u[i].im;
+  const double sv = sqrt(s2);
+  const double smax = group_reduce<N>(g, sv, OpMax());
+  const double smin = -group_reduce<N>(g, -sv, OpMax());
+  if (!(smax > 0.0) || !isfinite(smax)) {
+    cond = INFINITY;
+    rank = 0;
+    return;
+  }
+  rank = __popc(__ballot_sync(g.mask, sv > SINGULARITY_TOL * smax) & g.bits);
+  cond = (smin == 0.0) ? INFINITY : smax / smin;
 }
 
 struct EndpointArgs {
