@@ -283,6 +283,29 @@ def native_arm(args, prob):
     if traffic is not None:
         traffic = traffic * Pl / tpaths  # this rank's launch (the capture is the whole C5 launch)
 
+    clocks = clk.summary(ctx.local_rank) if ctx.rank == 0 else None
+    # The other two full-size configs (C3 stages, C4 membership), one timed step
+    # each through `--workload` in a child process, so that the driver's default
+    # run records them too; a failure there never touches the headline line.
+    other = None
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_other_workloads:
+        import subprocess
+
+        other = {}
+        for w in ("c3", "c4"):
+            try:
+                r = subprocess.run([sys.executable, os.path.abspath(__file__), "--workload", w, "--steps", "1",
+                                    "--warmup", "1"], capture_output=True, text=True, timeout=900)
+                d = json.loads(r.stdout.strip().splitlines()[-1])
+                keep = ("top_s", "cascade_s", "filter_s", "top_kernel_ms", "agree", "indeterminate", "degrees")
+                other[w] = {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
+                            "steps": d["steps"], "warmup": d["warmup"],
+                            "paths_per_step": d["config"]["paths_per_step"],
+                            "roofline_frac": (d.get("roofline") or {}).get("frac"),
+                            **{k: d["config"][k] for k in keep if k in d["config"]}}
+            except Exception as e:  # noqa: BLE001
+                other[w] = {"error": repr(e)[:300]}
+
     if ctx.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps,
@@ -292,7 +315,7 @@ def native_arm(args, prob):
                        "paths": P, "n": n, "seed": 5, "track_params": "reference defaults (tracker.py:113-127)",
                        "l2": "256 MB device fill before every step (> 126 MB L2); endpoint outputs 580 MB",
                        "finite_endpoints": finite, "parallelism": f"path shards x{ctx.world}"},
-            "clocks": clk.summary(ctx.local_rank),
+            "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -306,6 +329,7 @@ def native_arm(args, prob):
                          "counts_per_path": {"eval": ev / Pl, "jac": jc / Pl, "scale": sc / Pl},
                          "flop_model": fm.as_dict()},
             "cpu_baseline": cpu,
+            "other_workloads": other,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -420,6 +444,8 @@ def main():
     ap.add_argument("--workload", choices=["c5", "c3", "c4"], default="c5",
                     help="c5 (default, the headline config), c3 (top + cascade + filter), c4 (membership)")
     ap.add_argument("--c4-candidates", type=int, default=100000)
+    ap.add_argument("--no-other-workloads", action="store_true",
+                    help="skip the one-step C3 / C4 runs appended to the default line")
     args = ap.parse_args()
     from paper_1804_03807_b200 import configs
 
