@@ -50,7 +50,7 @@ NID_D void cdd_row(const HomDev& H, int row, const cdd (&x)[N], const cd* prm, c
       F[K] = a == 1 ? x[u] : cdd_mul(pw, x[u]);
       const dd aa = dd{(double)a, 0.0};
       D[K] = a == 1 ? pw : cdd{dd_mul(pw.re, aa), dd_mul(pw.im, aa)};
-      var[K] = u;
+      var[K] = u | (a == 1 ? 16 : 0);  // bit 4: D[K] is one
       ++K;
     }
     cdd p = cdd_from(c);
@@ -60,15 +60,20 @@ NID_D void cdd_row(const HomDev& H, int row, const cdd (&x)[N], const cd* prm, c
       p = cdd_mul(p, F[q]);
     }
     rv = cdd_add(rv, p);
+    // products with the constant one are skipped (they are exact in
+    // double-double, so the results are the same bit for bit): the derivative
+    // factor of an exponent-1 variable, the empty suffix of the last position
+    // and the suffix update after the first
     cdd sfx = one;
 #pragma unroll 1
     for (int q = K - 1; q >= 0; --q) {
-      const cdd d = cdd_mul(cdd_mul(P[q], D[q]), sfx);
-      const int u = var[q];
+      cdd d = (var[q] & 16) ? P[q] : cdd_mul(P[q], D[q]);
+      if (q < K - 1) d = cdd_mul(d, sfx);
+      const int u = var[q] & 15;
 #pragma unroll
       for (int j = 0; j < N; ++j)
         if (j == u) Jr[j] = cdd_add(Jr[j], d);
-      sfx = cdd_mul(sfx, F[q]);
+      if (q > 0) sfx = q == K - 1 ? F[q] : cdd_mul(sfx, F[q]);
     }
   }
 #pragma unroll
