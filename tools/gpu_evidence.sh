@@ -9,9 +9,9 @@ mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_${TAG}.log 2> gpurun_out/bench_${TAG}.err
 python bench.py --impl reference --steps 2 --warmup 1 --ref-sample 96 > gpurun_out/ref_arm_${TAG}.log 2>&1
 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29555 \
-  bench.py --gpus 1 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/torchrun_${TAG}.log 2>&1
+  bench.py --gpus 1 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-other-workloads > gpurun_out/torchrun_${TAG}.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
-  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launches_${TAG}.log 2>&1
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-other-workloads > gpurun_out/ncu_launches_${TAG}.log 2>&1
 python tools/probe_c5.py 200000 > gpurun_out/plain_probe_${TAG}.log 2>&1 && \
 ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_ops_dadd_dmul_dfma_pred_on.sum,smsp__thread_inst_executed.sum,smsp__inst_executed.sum,gpu__time_duration.sum \
   --clock-control none -k regex:track_ -c 1 --csv --log-file gpurun_out/opmix_${TAG}.csv \
