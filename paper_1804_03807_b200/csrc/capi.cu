@@ -833,7 +833,7 @@ static int track_impl(NidHomotopy* h, const NidTrackParams* prm, int P, const do
   // (the column-owner stream's descriptors when the table has one: track_col.cuh)
   const std::vector<uint4>& lruns = h->crec ? h->hcruns : h->hruns;
   for (size_t u = 0; u < lruns.size() && u < (size_t)NID_MAX_RUNS; ++u) a.runs_c[u] = lruns[u];
-  a.lat_slots = 8;
+  a.lat_slots = 4;  // (8 until the column-owner block pass: profiles/lat_slots_sweep_r02.log)
   if (getenv("NID_LAT_SLOTS")) a.lat_slots = atoi(getenv("NID_LAT_SLOTS"));
   if (!a.gstate) FAIL("out of device memory (slot state)");
 
