@@ -143,6 +143,19 @@ int nid_use_device(int i);
 int nid_homotopy_create(const NidHomotopyDesc* desc, NidHomotopy** out);
 int nid_homotopy_destroy(NidHomotopy* h);
 
+/* Host-only test hook (no device needed): lowers a term table into the
+ * column-owner stream that nid_homotopy_create builds for tables streamed from
+ * L2 (csrc/col_lower.h: the merged-monomial form of the reference's stacked
+ * evaluator, polynomials.py:202-256) for `groups` warps.  Copies up to
+ * cap_pieces 16-byte pieces (4 words each) and cap_runs run descriptors (4
+ * words each) and returns the full counts; cgrun / cgbase [17]: each warp's
+ * first run and first piece.  *eligible = 0 when the table does not take the
+ * stream (then nothing else is written).  tests/test_col_lower.py decodes the
+ * stream and checks it against the term table. */
+int nid_col_lower(const NidHomotopyDesc* desc, int groups, unsigned* pieces, long long cap_pieces,
+                  long long* n_pieces, unsigned* runs, long long cap_runs, long long* n_runs, int* cgrun,
+                  int* cgbase, int* eligible);
+
 /* Evaluate H, J and the noise scale at P points (host buffers):
  * x[P*n*2], t[P], params[P? per param_div] -> H[P*n*2], J[P*n*n*2] (row-major), scale[P]. */
 int nid_eval_batch(NidHomotopy* h, int P, const double* x, const double* t, const double* params,

@@ -23,7 +23,7 @@ EXPORTS = (
     "nid_homotopy_destroy", "nid_eval_batch", "nid_newton_step_batch", "nid_svd_batch",
     "nid_track_batch", "nid_track_batch_strided", "nid_last_counters", "nid_refine_batch", "nid_dd_refine_batch",
     "nid_match_pairs", "nid_track_cells", "nid_track_trace", "nid_init_devices", "nid_use_device",
-    "nid_compact_finite", "nid_gather_endpoints",
+    "nid_compact_finite", "nid_gather_endpoints", "nid_col_lower",
 )
 
 
@@ -101,6 +101,7 @@ def load_library():
             "nid_compact_finite": ([i, ll, p, p, ll, ll, p, p, ll, p, p], i),
             "nid_gather_endpoints": ([i, p, p, p, p, p, p, i, i, p, p, ll, p], i),
             "nid_last_counters": ([p], i),
+            "nid_col_lower": ([p, i, p, ll, p, p, ll, p, p, p, p], i),
             "nid_refine_batch": ([p, i, p, d, i, i, d, p, p, p, p, p], i),
             "nid_dd_refine_batch": ([p, i, p, i, p], i),
             "nid_match_pairs": ([i, i, i, p, p, ll, p], i),

@@ -626,6 +626,37 @@ int nid_homotopy_create(const NidHomotopyDesc* d, NidHomotopy** out) {
   return 0;
 }
 
+int nid_col_lower(const NidHomotopyDesc* d, int groups, unsigned* pieces, long long cap_pieces, long long* n_pieces,
+                  unsigned* runs, long long cap_runs, long long* n_runs, int* cgrun, int* cgbase, int* eligible) {
+  if (!d || !n_pieces || !n_runs || !cgrun || !cgbase || !eligible) FAIL("null argument");
+  if (d->n < 1 || d->n > NID_MAX_VARS || d->nterms < 0) FAIL("bad table shape");
+  if (groups < 1 || groups > 16) FAIL("groups must be in 1..16");
+  const int n = d->n, T = d->nterms;
+  std::vector<int> off(d->row_off, d->row_off + n + 1);
+  if (off[0] != 0 || off[n] != T) FAIL("row offsets do not cover the term table");
+  std::vector<double> acs(T), act(T);
+  for (int k = 0; k < T; ++k) {
+    acs[k] = hypot(d->coef_start[2 * k], d->coef_start[2 * k + 1]);
+    act[k] = hypot(d->coef_target[2 * k], d->coef_target[2 * k + 1]);
+  }
+  std::vector<uint4> pc, rn;
+  int gr[17], gb[17];
+  const bool ok = colhost::build(d, n, T, off, acs, act, groups, d->start_kind == 1, pc, rn, gr, gb);
+  *eligible = ok ? 1 : 0;
+  if (!ok) return 0;
+  *n_pieces = (long long)pc.size();
+  *n_runs = (long long)rn.size();
+  for (int w = 0; w < 17; ++w) {
+    cgrun[w] = gr[w];
+    cgbase[w] = gb[w];
+  }
+  if (pieces)
+    for (long long z = 0; z < (long long)pc.size() && z < cap_pieces; ++z) memcpy(pieces + 4 * z, &pc[z], 16);
+  if (runs)
+    for (long long z = 0; z < (long long)rn.size() && z < cap_runs; ++z) memcpy(runs + 4 * z, &rn[z], 16);
+  return 0;
+}
+
 int nid_homotopy_destroy(NidHomotopy* h) {
   if (!h) return 0;
   BIND_H(h);
